@@ -1,0 +1,480 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for the hot path of
+ * arXiv 2308.15152 (Ootomo & Yokota): FP32 GEMM emulated by an FP16 (or TF32)
+ * hi/lo split and three low-precision products (WMMAe-TCEC, §4.4).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2308_15152_b200/) never links, imports or calls it,
+ * and this file shares no code, header, table or constant generator with it.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; "S:n" = SPEC.md line n;
+ * "R#n" = reading n in DESIGN.md §3 (where the paper is silent or garbled).
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"):
+ *   orc_f32_to_f16      exhaustive over all 2^32 inputs vs numpy's float16 cast
+ *   orc_f32_to_tf32     exhaustive-by-class vs an independent float64 rint model
+ *   orc_split_*         SPEC worked vectors (tests/golden/split_vectors.txt),
+ *                       closed-form reconstruction exactness / {0,1 ulp} error
+ *   orc_emu_gemm        identity/permutation => reconstruct(split(B)) exactly,
+ *                       small-integer inputs => exact integer product, the
+ *                       componentwise error bound vs exact rational products,
+ *                       correction-off negative control (>= 32x worse),
+ *                       the paper's accuracy claim (<= FP32 SGEMM level)
+ *   orc_gemm_f64        exact integer product; numpy float64 matmul
+ *   orc_sgemm_f32       exact integer product; gamma_k |A||B| error bound
+ * Parity unpinned: none of the functions above.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -fPIC
+ *        -shared oracle.c -o liboracle.so -lm
+ * (-ffp-contract=off so that every a*b+c below is rounded exactly as written;
+ * fmaf() is called explicitly where a fused multiply-add is meant.)
+ */
+#include <stdint.h>
+#include <string.h>
+#include <math.h>
+#include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_MODE_FP16 0
+#define ORC_MODE_TF32 1
+
+static uint32_t bits_of(float x) { uint32_t u; memcpy(&u, &x, 4); return u; }
+static float float_of(uint32_t u) { float x; memcpy(&x, &u, 4); return x; }
+
+/* ------------------------------------------------------------------------ */
+/* toFP16: IEEE-754 binary32 -> binary16, round to nearest,  */
+/* ties to even (R#1), gradual underflow (R#3), overflow -> +-Inf (R#4).     */
+/* Written from the definition: x = sig * 2^E exactly; the binary16 quantum  */
+/* at |x| is 2^(floor(log2|x|) - 10), never below 2^-24 (the subnormal step).*/
+/* ------------------------------------------------------------------------ */
+uint16_t orc_f32_to_f16(float x)
+{
+    uint32_t u = bits_of(x);
+    uint16_t sign = (uint16_t)((u >> 16) & 0x8000u);
+    uint32_t bexp = (u >> 23) & 0xffu;
+    uint32_t frac = u & 0x7fffffu;
+
+    if (bexp == 0xffu) {                      /* Inf or NaN */
+        if (frac == 0) return (uint16_t)(sign | 0x7c00u);
+        return (uint16_t)(sign | 0x7e00u | (frac >> 13)); /* quiet NaN */
+    }
+    if (bexp == 0 && frac == 0) return sign;  /* +-0 */
+
+    /* exact value |x| = sig * 2^E, sig an integer < 2^24 */
+    uint64_t sig;
+    int E;
+    int e_unb;                                /* floor(log2|x|) */
+    if (bexp == 0) {                          /* binary32 subnormal */
+        sig = frac; E = -149;
+        e_unb = -127;                         /* < -126: far below 2^-24 */
+    } else {
+        sig = (1u << 23) | frac; E = (int)bexp - 150;
+        e_unb = (int)bexp - 127;
+    }
+    /* binary16 quantum exponent Q: 2^Q = ulp at |x| (normal) or 2^-24 */
+    int Q = (e_unb >= -14) ? (e_unb - 10) : -24;
+    uint64_t r;
+    if (Q <= E) {
+        r = sig << (E - Q);                   /* exact */
+    } else {
+        int shift = Q - E;
+        if (shift > 40) {
+            r = 0;                            /* |x| < 2^-25: rounds to 0 */
+        } else {
+            uint64_t rem = sig & ((1ull << shift) - 1ull);
+            uint64_t half = 1ull << (shift - 1);
+            r = sig >> shift;
+            if (rem > half || (rem == half && (r & 1ull))) r += 1;
+        }
+    }
+    /* value is r * 2^Q */
+    if (Q == -24) {
+        /* subnormal binade (or carry into the first normal, r == 1024, which
+           has exactly the same encoding 0x0400) */
+        return (uint16_t)(sign | (uint16_t)r);
+    }
+    int e16 = e_unb;
+    if (r == 2048) { r = 1024; e16 += 1; }    /* rounding carried */
+    if (e16 > 15) return (uint16_t)(sign | 0x7c00u); /* overflow -> Inf */
+    return (uint16_t)(sign | (uint16_t)((e16 + 15) << 10) | (uint16_t)(r - 1024));
+}
+
+/* toFP32: binary16 -> binary32, exact (binary16 is a subset). */
+float orc_f16_to_f32(uint16_t h)
+{
+    int s = (h >> 15) & 1;
+    int e = (h >> 10) & 31;
+    int m = h & 1023;
+    float v;
+    if (e == 31) {
+        if (m == 0) v = INFINITY;
+        else return float_of((s ? 0xffc00000u : 0x7fc00000u) | ((uint32_t)m << 13));
+    } else if (e == 0) {
+        v = ldexpf((float)m, -24);
+    } else {
+        v = ldexpf((float)(1024 + m), e - 25);
+    }
+    return s ? -v : v;
+}
+
+/* ------------------------------------------------------------------------ */
+/* TF32 (R#6): binary32 rounded to 10 fraction bits (11 significant bits),   */
+/* nearest-even, binary32 exponent range and subnormals kept; result is a    */
+/* binary32 bit pattern with the low 13 bits zero.  Overflow -> +-Inf.       */
+/* ------------------------------------------------------------------------ */
+float orc_f32_to_tf32(float x)
+{
+    uint32_t u = bits_of(x);
+    uint32_t sign = u & 0x80000000u;
+    uint32_t bexp = (u >> 23) & 0xffu;
+    uint32_t frac = u & 0x7fffffu;
+    if (bexp == 0xffu) {
+        if (frac == 0) return x;                                  /* +-Inf */
+        return float_of(sign | 0x7fc00000u | (frac & 0x7fe000u)); /* NaN */
+    }
+    /* the 24-bit (normal) or 23-bit (subnormal) significand, in units of
+       the binary32 ulp; keep the top 10 fraction bits: quantum = 2^13 ulps */
+    uint32_t sig = (bexp == 0) ? frac : ((1u << 23) | frac);
+    uint32_t r = sig >> 13;
+    uint32_t rem = sig & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (r & 1u))) r += 1;
+    if (bexp == 0) {
+        /* subnormal: r << 13 is the new fraction; r == 1024 becomes the
+           smallest normal, whose encoding is exactly 1 << 23 */
+        return float_of(sign | (r << 13));
+    }
+    uint32_t e = bexp;
+    if (r == 2048) { r = 1024; e += 1; }
+    if (e >= 0xffu) return float_of(sign | 0x7f800000u);         /* overflow */
+    return float_of(sign | (e << 23) | ((r - 1024) << 13));
+}
+
+/* ------------------------------------------------------------------------ */
+/* The split, Eqs. corr-1..corr-4.                              */
+/*   FP16: hi = toFP16(x);  lo = toFP16((x - toFP32(hi)) * 2^11)             */
+/*   TF32: hi = tf32(x);    lo = tf32(x - hi)          (R#6, no scale)       */
+/* x - toFP32(hi) is evaluated in binary32 as the paper writes it; it is     */
+/* exact (Sterbenz / hi == 0, R#2), so double evaluation would agree.        */
+/* ------------------------------------------------------------------------ */
+void orc_split_fp16(const float* x, int64_t count, uint16_t* hi, uint16_t* lo)
+{
+    #pragma omp parallel for schedule(static) if (count > 65536)
+    for (int64_t i = 0; i < count; ++i) {
+        uint16_t h = orc_f32_to_f16(x[i]);
+        float r = x[i] - orc_f16_to_f32(h);
+        float rs = r * 2048.0f;                  /* x 2^11 */
+        hi[i] = h;
+        lo[i] = orc_f32_to_f16(rs);
+    }
+}
+
+void orc_split_tf32(const float* x, int64_t count, float* hi, float* lo)
+{
+    #pragma omp parallel for schedule(static) if (count > 65536)
+    for (int64_t i = 0; i < count; ++i) {
+        float h = orc_f32_to_tf32(x[i]);
+        float r = x[i] - h;
+        hi[i] = h;
+        lo[i] = orc_f32_to_tf32(r);
+    }
+}
+
+/* reconstruct: hi + lo * 2^-11 (FP16) / hi + lo (TF32), in FP32 */
+void orc_reconstruct(int mode, const float* hi_val, const float* lo_val,
+                     int64_t count, float* out)
+{
+    for (int64_t i = 0; i < count; ++i) {
+        if (mode == ORC_MODE_FP16) out[i] = hi_val[i] + lo_val[i] * (1.0f / 2048.0f);
+        else out[i] = hi_val[i] + lo_val[i];
+    }
+}
+
+/* split one operand element and return the two parts as exact float values */
+static void split_value(int mode, float x, float* h, float* l)
+{
+    if (mode == ORC_MODE_FP16) {
+        uint16_t hh, ll;
+        orc_split_fp16(&x, 1, &hh, &ll);
+        *h = orc_f16_to_f32(hh);
+        *l = orc_f16_to_f32(ll);
+    } else {
+        orc_split_tf32(&x, 1, h, l);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Exact block sums for FP16 mode.  Every finite binary16 value is an        */
+/* integer multiple of 2^-24 below 2^16, so each product of two is an        */
+/* integer multiple of 2^-48 below 2^32: a sum of up to 2^60 of them is held */
+/* exactly in a 128-bit integer of 2^-48 units.                              */
+/* ------------------------------------------------------------------------ */
+typedef __int128 i128;
+
+static i128 units24(float v) { return (i128)(int64_t)ldexpf(v, 24); } /* exact */
+
+/* round S * 2^-48 to the nearest binary32, ties to even (one rounding) */
+static float i128_to_float_rn(i128 S)
+{
+    if (S == 0) return 0.0f;
+    int neg = S < 0;
+    unsigned __int128 a = neg ? (unsigned __int128)(-S) : (unsigned __int128)S;
+    int msb = 127;
+    while (!((a >> msb) & 1)) --msb;
+    float v;
+    if (msb <= 23) {
+        v = ldexpf((float)(uint32_t)a, -48);     /* exact */
+    } else {
+        int shift = msb - 23;
+        unsigned __int128 r = a >> shift;
+        unsigned __int128 rem = a & (((unsigned __int128)1 << shift) - 1);
+        unsigned __int128 half = (unsigned __int128)1 << (shift - 1);
+        if (rem > half || (rem == half && (r & 1))) r += 1;
+        v = ldexpf((float)(uint32_t)r, shift - 48); /* r <= 2^24: exact */
+    }
+    return neg ? -v : v;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O3: one output element of the emulation model (Eq. corr-5)     */
+/* with the outside-of-Tensor-Core combine of P:495 (R#7, R#8):              */
+/*   for each k-block b of kb:                                               */
+/*     P1_b   = sum_p hiA*hiB                  ("ideal" TC: exact, one RN)   */
+/*     corr_b = sum_p (loA*hiB + hiA*loB)      (same accumulator, R#8)        */
+/*     t      = RN(P1_b + corr_b * 2^-11)      (fmaf; 2^-11 -> 1 for TF32)   */
+/*     C      = RN(C + t)                      (ascending b)                 */
+/*   out = RN(alpha*C + RN(beta*C0))           (BLAS epilogue, R#17)         */
+/* corr_enable = 0 drops both correction products (policy "correction off",  */
+/* P:518-519) and is used only as a negative control.                        */
+/* ahi/alo: k parts of row i of A; bhi/blo: k parts of column j of B.        */
+/* ------------------------------------------------------------------------ */
+static float emu_element(int mode, int corr_enable, int k, int kb,
+                         const float* ahi, const float* alo,
+                         const float* bhi, const float* blo,
+                         float alpha, float beta, float c0, int read_c)
+{
+    const float scale = (mode == ORC_MODE_FP16) ? (1.0f / 2048.0f) : 1.0f;
+    float bc = read_c ? beta * c0 : 0.0f;
+    if (alpha == 0.0f || k == 0) return bc;   /* BLAS quick return: A, B unread */
+    float C = 0.0f;
+    for (int p0 = 0; p0 < k; p0 += kb) {
+        int p1 = p0 + kb < k ? p0 + kb : k;
+        float d_hi, d_corr;
+        int finite = 1;
+        for (int p = p0; p < p1; ++p)
+            if (!isfinite(ahi[p]) || !isfinite(alo[p]) ||
+                !isfinite(bhi[p]) || !isfinite(blo[p])) finite = 0;
+        if (mode == ORC_MODE_FP16 && finite) {
+            i128 s1 = 0, s2 = 0;
+            for (int p = p0; p < p1; ++p) {
+                s1 += units24(ahi[p]) * units24(bhi[p]);
+                if (corr_enable) {
+                    s2 += units24(alo[p]) * units24(bhi[p]);
+                    s2 += units24(ahi[p]) * units24(blo[p]);
+                }
+            }
+            d_hi = i128_to_float_rn(s1);
+            d_corr = i128_to_float_rn(s2);
+        } else {
+            /* TF32 parts (products of 11-bit significands are exact in
+               binary64) or non-finite FP16 operands: binary64 ascending sum,
+               then one rounding to binary32 */
+            double s1 = 0.0, s2 = 0.0;
+            for (int p = p0; p < p1; ++p) {
+                s1 += (double)ahi[p] * (double)bhi[p];
+                if (corr_enable) {
+                    s2 += (double)alo[p] * (double)bhi[p];
+                    s2 += (double)ahi[p] * (double)blo[p];
+                }
+            }
+            d_hi = (float)s1;
+            d_corr = (float)s2;
+        }
+        float t = fmaf(d_corr, scale, d_hi);
+        C = C + t;
+    }
+    return fmaf(alpha, C, bc);
+}
+
+/* gather the split parts of row i of A (column-major, lda) and column j of B */
+static void split_row(int mode, int k, const float* A, int64_t lda, int64_t i,
+                      float* h, float* l)
+{
+    for (int p = 0; p < k; ++p) split_value(mode, A[i + (int64_t)p * lda], &h[p], &l[p]);
+}
+static void split_col(int mode, int k, const float* B, int64_t ldb, int64_t j,
+                      float* h, float* l)
+{
+    for (int p = 0; p < k; ++p) split_value(mode, B[(int64_t)p + j * ldb], &h[p], &l[p]);
+}
+
+/*
+ * Batched emulated GEMM, column-major, BLAS conventions (R#17):
+ *   C_b = alpha * A_b B_b + beta * C_b,  X_b = X + b * strideX (elements).
+ * Eqs. corr-1..4 are applied to every operand first (the paper's order),
+ * then Eq. corr-5 per output element.  beta == 0 never reads C (R#19).
+ * Returns 0, or -1 on allocation failure.
+ */
+int orc_emu_gemm_batched(int mode, int corr_enable, int m, int n, int k, int kb,
+                         float alpha, const float* A, int64_t lda, int64_t strideA,
+                         const float* B, int64_t ldb, int64_t strideB,
+                         float beta, float* C, int64_t ldc, int64_t strideC,
+                         int batch)
+{
+    if (kb <= 0) kb = 64;
+    int64_t mk = (int64_t)m * k, kn = (int64_t)k * n;
+    float* ah = malloc(sizeof(float) * (mk > 0 ? mk : 1));
+    float* al = malloc(sizeof(float) * (mk > 0 ? mk : 1));
+    float* bh = malloc(sizeof(float) * (kn > 0 ? kn : 1));
+    float* bl = malloc(sizeof(float) * (kn > 0 ? kn : 1));
+    if (!ah || !al || !bh || !bl) { free(ah); free(al); free(bh); free(bl); return -1; }
+    for (int b = 0; b < batch; ++b) {
+        const float* Ab = A + (int64_t)b * strideA;
+        const float* Bb = B + (int64_t)b * strideB;
+        float* Cb = C + (int64_t)b * strideC;
+        /* Eqs. corr-1..corr-4: A_F16, dA_F16 stored row-wise (k contiguous) */
+        #pragma omp parallel for schedule(static)
+        for (int i = 0; i < m; ++i) split_row(mode, k, Ab, lda, i, ah + (int64_t)i * k, al + (int64_t)i * k);
+        #pragma omp parallel for schedule(static)
+        for (int j = 0; j < n; ++j) split_col(mode, k, Bb, ldb, j, bh + (int64_t)j * k, bl + (int64_t)j * k);
+        /* Eq. corr-5 */
+        #pragma omp parallel for schedule(static)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < m; ++i) {
+                float c0 = (beta != 0.0f) ? Cb[i + (int64_t)j * ldc] : 0.0f;
+                Cb[i + (int64_t)j * ldc] = emu_element(
+                    mode, corr_enable, k, kb, ah + (int64_t)i * k, al + (int64_t)i * k,
+                    bh + (int64_t)j * k, bl + (int64_t)j * k, alpha, beta, c0, beta != 0.0f);
+            }
+    }
+    free(ah); free(al); free(bh); free(bl);
+    return 0;
+}
+
+/*
+ * Selected output entries of one batched emulated GEMM (same definition as
+ * above; for sampled parity at full sizes).  Entry e is C_{bidx[e]}(ii[e], jj[e]);
+ * out[e] receives it (C itself is only read, for beta != 0).
+ */
+int orc_emu_gemm_entries(int mode, int corr_enable, int m, int n, int k, int kb,
+                         float alpha, const float* A, int64_t lda, int64_t strideA,
+                         const float* B, int64_t ldb, int64_t strideB,
+                         float beta, const float* C, int64_t ldc, int64_t strideC,
+                         int64_t nent, const int64_t* bidx, const int64_t* ii,
+                         const int64_t* jj, float* out)
+{
+    (void)m; (void)n;
+    if (kb <= 0) kb = 64;
+    int ok = 0;
+    #pragma omp parallel
+    {
+        size_t kk = (size_t)(k > 0 ? k : 1);
+        float* ah = malloc(sizeof(float) * kk);
+        float* al = malloc(sizeof(float) * kk);
+        float* bh = malloc(sizeof(float) * kk);
+        float* bl = malloc(sizeof(float) * kk);
+        if (!ah || !al || !bh || !bl) {
+            #pragma omp atomic write
+            ok = -1;
+        } else {
+            #pragma omp for schedule(dynamic, 4)
+            for (int64_t e = 0; e < nent; ++e) {
+                const float* Ab = A + bidx[e] * strideA;
+                const float* Bb = B + bidx[e] * strideB;
+                split_row(mode, k, Ab, lda, ii[e], ah, al);
+                split_col(mode, k, Bb, ldb, jj[e], bh, bl);
+                float c0 = (beta != 0.0f) ? C[bidx[e] * strideC + ii[e] + jj[e] * ldc] : 0.0f;
+                out[e] = emu_element(mode, corr_enable, k, kb, ah, al, bh, bl,
+                                     alpha, beta, c0, beta != 0.0f);
+            }
+        }
+        free(ah); free(al); free(bh); free(bl);
+    }
+    return ok;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O4: FP64 reference, R = alpha * sum_p a*b + beta * c in binary64,         */
+/* ascending p.  Output in binary64.                             */
+/* ------------------------------------------------------------------------ */
+void orc_gemm_f64_batched(int m, int n, int k, double alpha,
+                          const float* A, int64_t lda, int64_t strideA,
+                          const float* B, int64_t ldb, int64_t strideB,
+                          double beta, const float* C0, int64_t ldc, int64_t strideC,
+                          double* R, int64_t ldr, int64_t strideR, int batch)
+{
+    for (int b = 0; b < batch; ++b) {
+        const float* Ab = A + (int64_t)b * strideA;
+        const float* Bb = B + (int64_t)b * strideB;
+        #pragma omp parallel for schedule(static)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < m; ++i) {
+                double acc = 0.0;
+                for (int p = 0; p < k; ++p)
+                    acc += (double)Ab[i + (int64_t)p * lda] * (double)Bb[p + (int64_t)j * ldb];
+                double r = alpha * acc;
+                if (beta != 0.0) r += beta * (double)C0[(int64_t)b * strideC + i + (int64_t)j * ldc];
+                R[(int64_t)b * strideR + i + (int64_t)j * ldr] = r;
+            }
+    }
+}
+
+/* |A||B| in binary64 (for componentwise error bounds) */
+void orc_absgemm_f64(int m, int n, int k, const float* A, int64_t lda,
+                     const float* B, int64_t ldb, double* R, int64_t ldr)
+{
+    #pragma omp parallel for schedule(static)
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i < m; ++i) {
+            double acc = 0.0;
+            for (int p = 0; p < k; ++p)
+                acc += fabs((double)A[i + (int64_t)p * lda]) * fabs((double)B[p + (int64_t)j * ldb]);
+            R[i + (int64_t)j * ldr] = acc;
+        }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O5: plain FP32 SGEMM, the accuracy yardstick of the paper's claim         */
+/* ("same accuracy as cuBLAS SGEMM"): ascending p, one fused          */
+/* multiply-add per step, then out = RN(alpha*acc + RN(beta*c)).             */
+/* ------------------------------------------------------------------------ */
+void orc_sgemm_f32_batched(int m, int n, int k, float alpha,
+                           const float* A, int64_t lda, int64_t strideA,
+                           const float* B, int64_t ldb, int64_t strideB,
+                           float beta, float* C, int64_t ldc, int64_t strideC, int batch)
+{
+    for (int b = 0; b < batch; ++b) {
+        const float* Ab = A + (int64_t)b * strideA;
+        const float* Bb = B + (int64_t)b * strideB;
+        float* Cb = C + (int64_t)b * strideC;
+        #pragma omp parallel for schedule(static)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < m; ++i) {
+                float acc = 0.0f;
+                for (int p = 0; p < k; ++p)
+                    acc = fmaf(Ab[i + (int64_t)p * lda], Bb[p + (int64_t)j * ldb], acc);
+                float bc = (beta != 0.0f) ? beta * Cb[i + (int64_t)j * ldc] : 0.0f;
+                Cb[i + (int64_t)j * ldc] = fmaf(alpha, acc, bc);
+            }
+    }
+}
+
+int orc_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void orc_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
