@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the emulated SGEMM hot path (arXiv 2308.15152, WMMAe-TCEC on
+B200) -- the driver's contract:
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--mode fp16|tf32] [--config c2|c3]
+
+One "step" is one emu_sgemm_batched call over the whole workload (all §8(a)
+rows: fetch, split, three MMAs, per-k-block combine, epilogue), inputs
+resident in HBM.  Default workload: BASELINE.json configs[1] (c2: 1024 x
+(256x256x256) FP32, uniform[-1,1]) per GPU -- weak scaling over ranks, each
+rank running its own contiguous block of problems (no collective in the timed
+region).  Rank 0 prints ONE JSON line.  `--impl reference` times the CPU
+oracle (the reference arm of this tier) on a bounded sample of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "emulated SGEMM TFlop/s (1/2/4/8 B200) vs FP32 SIMT peak; rel. error vs FP64"
+UNIT = "TFlop/s"
+# B200 FP32 SIMT peak: 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz (max SM clock)
+FP32_SIMT_PEAK_TF = 148 * 128 * 2 * 1.965e9 / 1e12
+PAPER_A100 = {"value": 54.2, "unit": "TFlop/s", "hw": "A100 40GB SXM4", "fp32_simt_peak": 19.5,
+              "cite": "PAPER.md P:33, P:557"}
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="fp16", choices=["fp16", "tf32"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.002):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        try:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._t is not None:
+            self._stop.set()
+            self._t.join()
+            self._sample()
+
+    def summary(self):
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        rs = [name for bit, name in self.REASONS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": rs, "samples": len(self.samples)}
+
+
+def _traffic(config, mode):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        t = json.load(f)
+    v = t.get(f"{config}_{mode}")
+    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else None
+
+
+def _cpu_baseline(cfg, mode, A_host, B_host, budget_s=15.0):
+    """The oracle as it stands (emulation model O3), on this host's cores, on a
+    bounded sample of the same workload."""
+    import oracle
+    m, n, k = cfg.m, cfg.n, cfg.k
+    cores = oracle.max_threads()
+    if cfg.batch > 1:
+        t0 = time.perf_counter()
+        oracle.emu_gemm(mode, A_host[:1], B_host[:1], m, n, k)
+        t1 = time.perf_counter() - t0
+        cnt = int(max(1, min(cfg.batch, budget_s / max(t1, 1e-6))))
+        t0 = time.perf_counter()
+        oracle.emu_gemm(mode, A_host[:cnt], B_host[:cnt], m, n, k)
+        dt = time.perf_counter() - t0
+        flops = 2.0 * m * n * k * cnt
+        sample = f"{cnt} of {cfg.batch} problems ({m}x{n}x{k}), full oracle emulation model"
+    else:
+        # sampled entries of the single large GEMM
+        nent = 4096
+        g = workloads.rng(99)
+        ii = g.integers(0, m, nent)
+        jj = g.integers(0, n, nent)
+        bb = np.zeros(nent, dtype=np.int64)
+        t0 = time.perf_counter()
+        oracle.emu_gemm_entries(mode, A_host, B_host, m, n, k, bb, ii, jj)
+        dt = time.perf_counter() - t0
+        flops = 2.0 * k * nent
+        sample = f"{nent} sampled outputs of the {m}x{n}x{k} GEMM (full k each)"
+    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": sample, "seconds": round(dt, 3)}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed as it stands on host cores (rank 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    cfg = workloads.CONFIGS[args.config]
+    m, n, k = cfg.m, cfg.n, cfg.k
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if cfg.batch > 1:
+        A, B = workloads.make_operands(1, m, n, k, cfg.seed)
+        step = lambda: oracle.emu_gemm(args.mode, A, B, m, n, k)   # noqa: E731
+        flops = 2.0 * m * n * k
+        sample = f"each step: 1 of the {cfg.batch} problems ({m}x{n}x{k}) of the workload"
+    else:
+        A, B = workloads.make_operands(1, m, n, k, cfg.seed)
+        g = workloads.rng(99)
+        ii = g.integers(0, m, 256)
+        jj = g.integers(0, n, 256)
+        bb = np.zeros(256, dtype=np.int64)
+        step = lambda: oracle.emu_gemm_entries(args.mode, A, B, m, n, k, bb, ii, jj)  # noqa: E731
+        flops = 2.0 * k * 256
+        sample = f"each step: 256 sampled outputs (full k) of the {m}x{n}x{k} GEMM"
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = flops * args.steps / dt / 1e12
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": _config(cfg, args.mode, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def _config(cfg, mode, world):
+    return {"workload": f"{cfg.name}: {cfg.note}; {mode} split", "batch_per_gpu": cfg.batch,
+            "m": cfg.m, "n": cfg.n, "k": cfg.k, "split": mode, "inputs": "uniform[-1,1] FP32, seeded Philox",
+            "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
+            "l2": "no flush: inputs per step exceed the 126 MB L2" if
+                  4 * (cfg.m * cfg.k + cfg.k * cfg.n + cfg.m * cfg.n) * cfg.batch > 126e6 else "small"}
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2308_15152_b200 as emu
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workloads.CONFIGS[args.config]
+    m, n, k, batch = cfg.m, cfg.n, cfg.k, cfg.batch
+    mode = args.mode
+
+    # inputs: this rank's contiguous block of problems (weak scaling)
+    A_h, B_h = workloads.make_operands(batch, m, n, k, cfg.seed, item0=rank * batch)
+    dA = torch.from_numpy(A_h).cuda()
+    dB = torch.from_numpy(B_h).cuda()
+    dC = torch.empty((batch, n, m), device="cuda")
+    stream = torch.cuda.current_stream()
+    sA, sB, sC = k * m, n * k, n * m
+
+    launches = 0
+
+    def step():
+        nonlocal launches
+        emu.emu_sgemm_batched(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, stream)
+        launches += emu.emu_last_launch_count()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    flops_step = 2.0 * m * n * k * batch * world
+    value = flops_step * args.steps / (ms_max / 1e3) / 1e12
+    ms_per_step = ms_max / args.steps
+
+    # accuracy on sampled problems of this rank (outside the timed region)
+    import oracle
+    idx = [0, batch // 2, batch - 1] if batch > 1 else [0]
+    if batch > 1:
+        C_s = dC[idx].cpu().numpy()
+        R = oracle.gemm_f64(A_h[idx], B_h[idx], m, n, k)
+        S = oracle.sgemm_f32(A_h[idx], B_h[idx], m, n, k)
+        e_emu, e_sg = oracle.rel_frobenius(C_s, R), oracle.rel_frobenius(S, R)
+        acc_note = f"{len(idx)} problems"
+    else:
+        g = workloads.rng(5)
+        ii, jj = g.integers(0, m, 512), g.integers(0, n, 512)
+        got = dC[0][torch.from_numpy(jj), torch.from_numpy(ii)].cpu().numpy().astype(np.float64)
+        R = np.array([np.dot(A_h[0, :, i].astype(np.float64), B_h[0, j, :].astype(np.float64)) for i, j in zip(ii, jj)])
+        e_emu = float(np.linalg.norm(got - R) / np.linalg.norm(R))
+        e_sg = None
+        acc_note = "512 sampled outputs"
+
+    # e2e through the C ABI with pinned HOST buffers (H2D + compute + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        pA = torch.from_numpy(A_h).pin_memory()
+        pB = torch.from_numpy(B_h).pin_memory()
+        pC = torch.empty((batch, n, m)).pin_memory()
+        emu.emu_sgemm_batched_host(m, n, k, 1.0, pA, m, sA, pB, k, sB, 0.0, pC, m, sC, batch, mode, stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            emu.emu_sgemm_batched_host(m, n, k, 1.0, pA, m, sA, pB, k, sB, 0.0, pC, m, sC, batch, mode, stream)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops_step * args.e2e_steps / float(dt.item()) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int(pA.numel() * 4 + pB.numel() * 4),
+               "d2h_bytes_per_step": int(pC.numel() * 4), "steps": args.e2e_steps,
+               "api": "emu_sgemm_batched_host (pinned host buffers)"}
+
+    peaks = _peaks()
+    tc_peak = peaks["bf16_tflops"] * (1.0 if mode == "fp16" else 0.5)   # fp16 = bf16 rate; tf32 = 1/2 (nominal ratio)
+    if args.config == "c2":
+        bytes_launch = 4.0 * (m * k + k * n + m * n) * batch
+        achieved = bytes_launch / (ms_per_step / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(args.config, mode),
+                "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peaks["source"],
+                "kernel": "emu_sgemm_kernel"}
+    else:
+        tc_flops = 6.0 * m * n * k * batch
+        achieved = tc_flops / (ms_per_step / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": achieved / tc_peak, "traffic": _traffic(args.config, mode),
+                "algorithmic_flops_per_launch": tc_flops, "peak_source": peaks["source"] +
+                (" (bf16 peak; fp16 same rate)" if mode == "fp16" else " (bf16 peak x 1/2 nominal tf32 ratio)"),
+                "kernel": "emu_sgemm_kernel"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline(cfg, mode, A_h, B_h)
+
+    per_gpu = value / world
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config(cfg, mode, world),
+        "frac_fp32_simt_peak": per_gpu / FP32_SIMT_PEAK_TF,
+        "frac_tc_peak_over_3": per_gpu / (tc_peak / 3.0),
+        "rel_frobenius_vs_fp64": e_emu, "rel_frobenius_fp32_sgemm": e_sg, "accuracy_sample": acc_note,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk.summary(), "paper_context": PAPER_A100,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * emu_sgemm.h -- C ABI of the B200 (sm_100a) emulated SGEMM library
+ * (libemusgemm.so), the hot path of arXiv 2308.15152 (Ootomo & Yokota,
+ * "Reducing shared memory footprint to leverage high throughput on Tensor
+ * Cores and its flexible API extension library", §4.4 "WMMAe-TCEC").
+ *
+ * What is computed (citations: P:n = /root/reference/PAPER.md line n;
+ * R#n = reading n in DESIGN.md §3):
+ *   The paper computes C_F32 = A_F32 B_F32 as
+ *     A_F16  = toFP16(A_F32)                                   Eq. corr-1
+ *     dA_F16 = toFP16((A_F32 - toFP32(A_F16)) * 2^11)          Eq. corr-2
+ *     (same for B)                                             Eqs. corr-3/4
+ *     C = A_F16 B_F16 + (dA_F16 B_F16 + A_F16 dB_F16) / 2^11   Eq. corr-5
+ *   with the accumulation moved outside the Tensor Core's RZ rounding:
+ *   the main product and the two correction products are accumulated in two
+ *   separate tensor-core accumulators over one k-block of KB elements, then
+ *   combined in FP32 round-to-nearest on CUDA cores, t = RN(D_hi + D_corr*2^-11),
+ *   C_acc = RN(C_acc + t), block after block (R#7, R#8).  EMU_SPLIT_TF32 is the
+ *   TF32 hi/lo variant of north_star (R#6: hi = RNE_tf32(x), lo = RNE_tf32(x-hi),
+ *   scale 1).  Finally C = RN(alpha*C_acc + RN(beta*C)) (BLAS, R#17); beta == 0
+ *   never reads C (R#19).  The batched form runs `batch` independent problems
+ *   (P:552): X_b = X + b*strideX for X in {A, B, C}.
+ *
+ * Conventions: column-major throughout, no transposes (A(i,p) = A[i + p*lda],
+ * m x k; B(p,j) = B[p + j*ldb], k x n; C(i,j) = C[i + j*ldc], m x n).  All
+ * pointers are DEVICE pointers owned by the caller (except the _host entry),
+ * all sizes are elements.  `stream` is a cudaStream_t (NULL = legacy default
+ * stream); every call is asynchronous on it unless stated.  Results are
+ * deterministic: identical inputs and configuration give bit-identical C
+ * (no split-K, no atomics on C).
+ *
+ * Errors: arguments are validated synchronously before anything is launched;
+ * on any non-SUCCESS return C is untouched.  Faults during kernel execution
+ * surface as CUDA errors at the caller's next synchronisation.
+ *
+ * Memory: the device entries allocate no global memory (tensor memory is
+ * allocated and freed inside each CTA); per-device attributes are cached.
+ * Thread-safe.  sm_100a only (B200); other devices -> EMU_STATUS_ARCH_MISMATCH.
+ */
+#ifndef EMU_SGEMM_H_
+#define EMU_SGEMM_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    EMU_SPLIT_FP16 = 0, /* FP16 hi + 2^11-scaled FP16 lo, kind::f16 MMAs */
+    EMU_SPLIT_TF32 = 1  /* TF32 hi + TF32 lo, kind::tf32 MMAs (north_star, R#6)    */
+} emu_split_mode;
+
+typedef enum {
+    EMU_STATUS_SUCCESS = 0,
+    EMU_STATUS_INVALID_VALUE = 1,  /* a size, leading dimension, stride, pointer or mode is invalid */
+    EMU_STATUS_NOT_SUPPORTED = 2,  /* valid BLAS call outside this version's domain (see below)     */
+    EMU_STATUS_ARCH_MISMATCH = 3,  /* current device is not sm_100                                  */
+    EMU_STATUS_LAUNCH_FAILED = 4,  /* kernel launch returned an error                               */
+    EMU_STATUS_CUDA_ERROR = 5      /* another CUDA runtime/driver call failed                       */
+} emu_status;
+
+/* Flags for emu_sgemm_batched_ex. */
+#define EMU_FLAG_NO_CORRECTION 1u  /* policy "error correction off": drop both
+                                      correction products; a negative control only */
+
+/*
+ * emu_sgemm_batched -- C_b = alpha * A_b B_b + beta * C_b for b in [0, batch).
+ *   m, n, k, batch >= 0; lda >= max(1, m); ldb >= max(1, k); ldc >= max(1, m).
+ *   strideA / strideB may be 0 (one operand shared by every problem); strideC
+ *   must make the outputs disjoint when batch > 1 (|strideC| >= ldc*n).
+ *   A and B may be NULL only when they are not read (k == 0 or alpha == 0);
+ *   C may be NULL only when m == 0, n == 0 or batch == 0.  C must not
+ *   overlap A or B.
+ *   Quick returns: m == 0 || n == 0 || batch == 0 -> SUCCESS, nothing
+ *   launched; k == 0 || alpha == 0 -> C = RN(beta*C) (beta == 0 writes +0).
+ *   Domain (else NOT_SUPPORTED): A, B 16-byte aligned; lda, ldb, strideA,
+ *   strideB multiples of 4 elements (tensor-map strides are 16-byte units).
+ *   FP16 mode: |A|, |B| < 65520 and finite, else those outputs are
+ *   non-finite (R#4); pass d_range_flag to emu_sgemm_batched_ex to detect it.
+ */
+emu_status emu_sgemm_batched(int m, int n, int k, float alpha,
+                             const float* A, int lda, long long strideA,
+                             const float* B, int ldb, long long strideB,
+                             float beta, float* C, int ldc, long long strideC,
+                             int batch, emu_split_mode mode, void* stream);
+
+/* emu_sgemm -- the single-problem form (batch = 1). */
+emu_status emu_sgemm(int m, int n, int k, float alpha,
+                     const float* A, int lda, const float* B, int ldb,
+                     float beta, float* C, int ldc, emu_split_mode mode, void* stream);
+
+/*
+ * emu_sgemm_batched_ex -- emu_sgemm_batched plus:
+ *   d_range_flag: NULL, or a device unsigned int that the kernel ORs with 1
+ *     (sticky, never cleared) when an FP16-mode operand element has
+ *     |x| >= 65520 or is not finite (its hi part is +-Inf/NaN, R#4);
+ *   kblock: the combine interval KB in k (0 = default 64; otherwise a positive
+ *     multiple of 32, at most 4096);
+ *   flags: EMU_FLAG_* bits (0 = the paper's method).
+ */
+emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha,
+                                const float* A, int lda, long long strideA,
+                                const float* B, int ldb, long long strideB,
+                                float beta, float* C, int ldc, long long strideC,
+                                int batch, emu_split_mode mode, void* stream,
+                                unsigned int* d_range_flag, int kblock, unsigned int flags);
+
+/*
+ * emu_sgemm_batched_host -- the same operation on HOST buffers (pinned or
+ * pageable, column-major as above, C read only if beta != 0): stages the
+ * operands into device memory it allocates on `stream`, runs the device path,
+ * copies C back and synchronises `stream` before returning.  Copies and
+ * compute run in stream order.  Same domain and errors;
+ * allocation failure -> EMU_STATUS_CUDA_ERROR.
+ */
+emu_status emu_sgemm_batched_host(int m, int n, int k, float alpha,
+                                  const float* A, int lda, long long strideA,
+                                  const float* B, int ldb, long long strideB,
+                                  float beta, float* C, int ldc, long long strideC,
+                                  int batch, emu_split_mode mode, void* stream);
+
+/*
+ * emu_split -- the split of Eqs. corr-1..corr-4 (FP16: P:481-488) or R#6
+ * (TF32), elementwise over `count` contiguous device floats, with the SAME
+ * device code the GEMM kernels use for operand staging.  FP16: hi and lo are
+ * device arrays of `count` uint16 binary16 bit patterns.  TF32: hi and lo are
+ * device arrays of `count` float (binary32 patterns with the low 13 bits 0).
+ * count >= 0; x, hi, lo non-NULL when count > 0 and 4-byte aligned.
+ */
+emu_status emu_split(const float* x, long long count, emu_split_mode mode,
+                     void* hi, void* lo, void* stream);
+
+/* Number of kernel launches the last successful call on this host thread
+ * issued (0 for a quick return without a scale kernel); for launch accounting. */
+int emu_last_launch_count(void);
+
+/* Human-readable status. Never NULL. */
+const char* emu_status_string(emu_status status);
+
+/* Library version: major*10000 + minor*100 + patch. */
+int emu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EMU_SGEMM_H_ */

@@ -1,0 +1,140 @@
+"""Python binding of libemusgemm.so -- the B200 emulated-SGEMM C ABI
+(include/emu_sgemm.h).  Argument marshalling only: every step of the method
+runs in the library's sm_100a kernels.  There is no fallback: if the library
+is missing this import fails.
+
+Functions keep the C names and argument order; pointer arguments accept a
+torch tensor (its data_ptr()), an int address or None.  `stream` defaults to
+torch's current CUDA stream.  A non-SUCCESS status raises EmuError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "EMU_SPLIT_FP16", "EMU_SPLIT_TF32", "EMU_FLAG_NO_CORRECTION", "EmuError", "lib", "LIB_PATH",
+    "emu_sgemm", "emu_sgemm_batched", "emu_sgemm_batched_ex", "emu_sgemm_batched_host",
+    "emu_split", "emu_status_string", "emu_version", "emu_last_launch_count", "mode_of",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libemusgemm.so")
+
+EMU_SPLIT_FP16 = 0
+EMU_SPLIT_TF32 = 1
+EMU_FLAG_NO_CORRECTION = 1
+STATUS = {0: "SUCCESS", 1: "INVALID_VALUE", 2: "NOT_SUPPORTED", 3: "ARCH_MISMATCH",
+          4: "LAUNCH_FAILED", 5: "CUDA_ERROR"}
+
+
+class EmuError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: EMU_STATUS_{STATUS.get(status, status)}")
+        self.status = status
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2308_15152_b200.build` "
+                      "(or __graft_entry__.build()). There is no CPU fallback.")
+
+lib = ctypes.CDLL(LIB_PATH)
+_i = ctypes.c_int
+_ll = ctypes.c_longlong
+_f = ctypes.c_float
+_p = ctypes.c_void_p
+_u = ctypes.c_uint
+
+_GEMM_ARGS = [_i, _i, _i, _f, _p, _i, _ll, _p, _i, _ll, _f, _p, _i, _ll, _i, _i, _p]
+lib.emu_sgemm_batched.argtypes = _GEMM_ARGS
+lib.emu_sgemm_batched.restype = _i
+lib.emu_sgemm_batched_ex.argtypes = _GEMM_ARGS + [_p, _i, _u]
+lib.emu_sgemm_batched_ex.restype = _i
+lib.emu_sgemm_batched_host.argtypes = _GEMM_ARGS
+lib.emu_sgemm_batched_host.restype = _i
+lib.emu_sgemm.argtypes = [_i, _i, _i, _f, _p, _i, _p, _i, _f, _p, _i, _i, _p]
+lib.emu_sgemm.restype = _i
+lib.emu_split.argtypes = [_p, _ll, _i, _p, _p, _p]
+lib.emu_split.restype = _i
+lib.emu_status_string.argtypes = [_i]
+lib.emu_status_string.restype = ctypes.c_char_p
+lib.emu_version.argtypes = []
+lib.emu_version.restype = _i
+lib.emu_last_launch_count.argtypes = []
+lib.emu_last_launch_count.restype = _i
+
+
+def mode_of(mode) -> int:
+    if mode in (EMU_SPLIT_FP16, "fp16"):
+        return EMU_SPLIT_FP16
+    if mode in (EMU_SPLIT_TF32, "tf32"):
+        return EMU_SPLIT_TF32
+    return int(mode)  # let the library reject it
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):          # numpy array (host entry)
+        return x.ctypes.data
+    raise TypeError(type(x))
+
+
+def _stream(s):
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise EmuError(st, where)
+
+
+def emu_sgemm_batched(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+                      batch, mode, stream=None):
+    _check(lib.emu_sgemm_batched(m, n, k, alpha, _ptr(A), lda, strideA, _ptr(B), ldb, strideB,
+                                 beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream)),
+           "emu_sgemm_batched")
+
+
+def emu_sgemm_batched_ex(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+                         batch, mode, stream=None, range_flag=None, kblock=0, flags=0):
+    _check(lib.emu_sgemm_batched_ex(m, n, k, alpha, _ptr(A), lda, strideA, _ptr(B), ldb, strideB,
+                                    beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream),
+                                    _ptr(range_flag), kblock, flags),
+           "emu_sgemm_batched_ex")
+
+
+def emu_sgemm_batched_host(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+                           batch, mode, stream=None):
+    _check(lib.emu_sgemm_batched_host(m, n, k, alpha, _ptr(A), lda, strideA, _ptr(B), ldb, strideB,
+                                      beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream)),
+           "emu_sgemm_batched_host")
+
+
+def emu_sgemm(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, mode, stream=None):
+    _check(lib.emu_sgemm(m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb, beta, _ptr(C), ldc,
+                         mode_of(mode), _stream(stream)), "emu_sgemm")
+
+
+def emu_split(x, count, mode, hi, lo, stream=None):
+    _check(lib.emu_split(_ptr(x), count, mode_of(mode), _ptr(hi), _ptr(lo), _stream(stream)), "emu_split")
+
+
+def emu_status_string(status: int) -> str:
+    return lib.emu_status_string(status).decode()
+
+
+def emu_version() -> int:
+    return lib.emu_version()
+
+
+def emu_last_launch_count() -> int:
+    return lib.emu_last_launch_count()

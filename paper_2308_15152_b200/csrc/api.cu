@@ -1,0 +1,369 @@
+// api.cu -- the C ABI of libemusgemm.so (declared and documented in
+// include/emu_sgemm.h): argument validation, tensor-map encoding, launch.
+// Every arithmetic step of the method runs in the kernels of this library.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "emu_sgemm.h"
+#include "gemm_sm100.cuh"
+#include "split.cuh"
+
+#define EMU_VERSION 100  // 0.1.0
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+struct DeviceInfo {
+    int ok = -1;  // -1 unknown, 0 not sm_100, 1 sm_100
+    int sms = 0;
+    bool attr_set[2] = {false, false};
+};
+
+constexpr int kMaxDevices = 64;
+DeviceInfo g_dev[kMaxDevices];
+std::mutex g_dev_mu;
+
+emu_status device_check(int& dev, int& sms)
+{
+    if (cudaGetDevice(&dev) != cudaSuccess) return EMU_STATUS_CUDA_ERROR;
+    if (dev < 0 || dev >= kMaxDevices) return EMU_STATUS_CUDA_ERROR;
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DeviceInfo& d = g_dev[dev];
+    if (d.ok < 0) {
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            return EMU_STATUS_CUDA_ERROR;
+        d.ok = (major == 10 && minor == 0) ? 1 : 0;
+    }
+    sms = d.sms;
+    return d.ok == 1 ? EMU_STATUS_SUCCESS : EMU_STATUS_ARCH_MISMATCH;
+}
+
+template <int MODE, int BN>
+emu_status ensure_smem_attr(int dev)
+{
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_dev[dev].attr_set[MODE]) return EMU_STATUS_SUCCESS;
+    if (cudaFuncSetAttribute(emu::emu_sgemm_kernel<MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)emu::GemmCfg<MODE, BN>::SMEM_BYTES) != cudaSuccess)
+        return EMU_STATUS_CUDA_ERROR;
+    g_dev[dev].attr_set[MODE] = true;
+    return EMU_STATUS_SUCCESS;
+}
+
+// 3-D FP32 tensor map {dim0 contiguous, dim1, batch}
+bool make_map(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t ld,
+              uint64_t nbatch, uint64_t bstride, uint32_t box0, uint32_t box1, CUtensorMapSwizzle sw)
+{
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {d0, d1, nbatch};
+    cuuint64_t strides[2] = {ld * 4, bstride * 4};
+    cuuint32_t box[3] = {box0, box1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// k == 0 or alpha == 0: C = RN(beta*C) (beta == 0 writes +0 and never reads C)
+__global__ void scale_c_kernel(float* C, int m, int n, long long ldc, long long strideC, int batch, float beta)
+{
+    const long long cols = (long long)n * batch;
+    for (long long cj = blockIdx.x; cj < cols; cj += gridDim.x) {
+        const long long b = cj / n, j = cj - b * n;
+        float* col = C + b * strideC + j * ldc;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) col[i] = beta != 0.0f ? __fmul_rn(beta, col[i]) : 0.0f;
+    }
+}
+
+__global__ void split_fp16_kernel(const float* __restrict__ x, long long count, uint16_t* __restrict__ hi,
+                                  uint16_t* __restrict__ lo)
+{
+    const long long pairs = count / 2;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride) {
+        const float2 v = reinterpret_cast<const float2*>(x)[i];
+        uint32_t h, l;
+        emu::split_fp16x2(v.x, v.y, h, l);
+        reinterpret_cast<uint32_t*>(hi)[i] = h;
+        reinterpret_cast<uint32_t*>(lo)[i] = l;
+    }
+    if ((count & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        uint32_t h, l;
+        emu::split_fp16x2(x[count - 1], 0.0f, h, l);
+        hi[count - 1] = (uint16_t)(h & 0xffffu);
+        lo[count - 1] = (uint16_t)(l & 0xffffu);
+    }
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ x, long long count, uint32_t* __restrict__ hi,
+                                  uint32_t* __restrict__ lo)
+{
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        uint32_t h, l;
+        emu::split_tf32(x[i], h, l);
+        hi[i] = h;
+        lo[i] = l;
+    }
+}
+
+emu_status launch_status(cudaError_t e)
+{
+    if (e == cudaSuccess) return EMU_STATUS_SUCCESS;
+    return EMU_STATUS_LAUNCH_FAILED;
+}
+
+template <int MODE>
+emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
+                    const float* B, int ldb, long long strideB, float beta, float* C, int ldc, long long strideC,
+                    int batch, cudaStream_t stream, unsigned* range_flag, int kblock, unsigned flags)
+{
+    constexpr int BN = 128;
+    using Cfg = emu::GemmCfg<MODE, BN>;
+    emu_status st = ensure_smem_attr<MODE, BN>(dev);
+    if (st != EMU_STATUS_SUCCESS) return st;
+
+    const bool a_b = batch > 1 && strideA != 0;
+    const bool b_b = batch > 1 && strideB != 0;
+    CUtensorMap tmA, tmB;
+    // dim-2 stride: any valid value when the batch extent is 1
+    const uint64_t sA = a_b ? (uint64_t)strideA : (((uint64_t)lda * (uint64_t)k + 3) & ~uint64_t(3));
+    const uint64_t sB = b_b ? (uint64_t)strideB : (((uint64_t)ldb * (uint64_t)n + 3) & ~uint64_t(3));
+    if (!make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA, Cfg::BM, Cfg::BK,
+                  CU_TENSOR_MAP_SWIZZLE_NONE))
+        return EMU_STATUS_NOT_SUPPORTED;
+    if (!make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB, Cfg::BK, BN,
+                  CU_TENSOR_MAP_SWIZZLE_128B))
+        return EMU_STATUS_NOT_SUPPORTED;
+
+    emu::GemmParams p;
+    p.m = m; p.n = n; p.k = k;
+    p.a_batched = a_b; p.b_batched = b_b;
+    p.alpha = alpha; p.beta = beta;
+    p.C = C; p.ldc = ldc; p.strideC = strideC;
+    p.tiles_m = (m + Cfg::BM - 1) / Cfg::BM;
+    p.tiles_n = (n + BN - 1) / BN;
+    p.num_tiles = (long long)p.tiles_m * p.tiles_n * batch;
+    p.num_k_stages = (k + Cfg::BK - 1) / Cfg::BK;
+    p.kb_stages = (kblock > 0 ? kblock : 64) / Cfg::BK;
+    p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
+    p.range_flag = MODE == 0 ? range_flag : nullptr;
+
+    const long long grid = std::min<long long>(p.num_tiles, sms);
+    emu::emu_sgemm_kernel<MODE, BN><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, p);
+    g_last_launches = 1;
+    return launch_status(cudaGetLastError());
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+__attribute__((visibility("default"))) const char* emu_status_string(emu_status s)
+{
+    switch (s) {
+        case EMU_STATUS_SUCCESS: return "EMU_STATUS_SUCCESS";
+        case EMU_STATUS_INVALID_VALUE: return "EMU_STATUS_INVALID_VALUE";
+        case EMU_STATUS_NOT_SUPPORTED: return "EMU_STATUS_NOT_SUPPORTED";
+        case EMU_STATUS_ARCH_MISMATCH: return "EMU_STATUS_ARCH_MISMATCH";
+        case EMU_STATUS_LAUNCH_FAILED: return "EMU_STATUS_LAUNCH_FAILED";
+        case EMU_STATUS_CUDA_ERROR: return "EMU_STATUS_CUDA_ERROR";
+    }
+    return "EMU_STATUS_UNKNOWN";
+}
+
+__attribute__((visibility("default"))) int emu_version(void) { return EMU_VERSION; }
+
+__attribute__((visibility("default"))) int emu_last_launch_count(void) { return g_last_launches; }
+
+__attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
+                                const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
+                                long long strideC, int batch, emu_split_mode mode, void* stream,
+                                unsigned int* d_range_flag, int kblock, unsigned int flags)
+{
+    g_last_launches = 0;
+    // ---- synchronous validation (C untouched on error) ----
+    if (m < 0 || n < 0 || k < 0 || batch < 0) return EMU_STATUS_INVALID_VALUE;
+    if (mode != EMU_SPLIT_FP16 && mode != EMU_SPLIT_TF32) return EMU_STATUS_INVALID_VALUE;
+    if (lda < std::max(1, m) || ldb < std::max(1, k) || ldc < std::max(1, m)) return EMU_STATUS_INVALID_VALUE;
+    if (strideA < 0 || strideB < 0 || strideC < 0) return EMU_STATUS_INVALID_VALUE;
+    if (kblock < 0 || (kblock > 0 && (kblock % 32 != 0 || kblock > 4096))) return EMU_STATUS_INVALID_VALUE;
+    if (flags & ~EMU_FLAG_NO_CORRECTION) return EMU_STATUS_INVALID_VALUE;
+    if (m == 0 || n == 0 || batch == 0) return EMU_STATUS_SUCCESS;
+    if (C == nullptr) return EMU_STATUS_INVALID_VALUE;
+    if (batch > 1 && strideC < (long long)ldc * n) return EMU_STATUS_INVALID_VALUE;
+    const bool reads_ab = k > 0 && alpha != 0.0f;
+    if (reads_ab && (A == nullptr || B == nullptr)) return EMU_STATUS_INVALID_VALUE;
+
+    int dev = 0, sms = 0;
+    emu_status st = device_check(dev, sms);
+    if (st != EMU_STATUS_SUCCESS) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+    if (!reads_ab) {
+        const long long cols = (long long)n * batch;
+        const unsigned grid = (unsigned)std::min<long long>(cols, 65535LL * 8);
+        scale_c_kernel<<<grid, 256, 0, s>>>(C, m, n, ldc, strideC, batch, beta);
+        g_last_launches = 1;
+        return launch_status(cudaGetLastError());
+    }
+    // ---- domain of the TMA path ----
+    if (!aligned16(A) || !aligned16(B)) return EMU_STATUS_NOT_SUPPORTED;
+    if (lda % 4 != 0 || ldb % 4 != 0) return EMU_STATUS_NOT_SUPPORTED;
+    if ((batch > 1 && strideA % 4 != 0) || (batch > 1 && strideB % 4 != 0)) return EMU_STATUS_NOT_SUPPORTED;
+    if ((unsigned long long)strideA * 4 >= (1ull << 40) || (unsigned long long)strideB * 4 >= (1ull << 40))
+        return EMU_STATUS_NOT_SUPPORTED;
+
+    if (mode == EMU_SPLIT_FP16)
+        return run_gemm<0>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch,
+                           s, d_range_flag, kblock, flags);
+    return run_gemm<1>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, s,
+                       nullptr, kblock, flags);
+}
+
+__attribute__((visibility("default"))) emu_status emu_sgemm_batched(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
+                             const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
+                             long long strideC, int batch, emu_split_mode mode, void* stream)
+{
+    return emu_sgemm_batched_ex(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch,
+                                mode, stream, nullptr, 0, 0u);
+}
+
+__attribute__((visibility("default"))) emu_status emu_sgemm(int m, int n, int k, float alpha, const float* A, int lda, const float* B, int ldb, float beta,
+                     float* C, int ldc, emu_split_mode mode, void* stream)
+{
+    return emu_sgemm_batched_ex(m, n, k, alpha, A, lda, 0, B, ldb, 0, beta, C, ldc, 0, 1, mode, stream, nullptr, 0,
+                                0u);
+}
+
+__attribute__((visibility("default"))) emu_status emu_split(const float* x, long long count, emu_split_mode mode, void* hi, void* lo, void* stream)
+{
+    g_last_launches = 0;
+    if (count < 0) return EMU_STATUS_INVALID_VALUE;
+    if (mode != EMU_SPLIT_FP16 && mode != EMU_SPLIT_TF32) return EMU_STATUS_INVALID_VALUE;
+    if (count == 0) return EMU_STATUS_SUCCESS;
+    if (!x || !hi || !lo) return EMU_STATUS_INVALID_VALUE;
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 3u)
+        return EMU_STATUS_INVALID_VALUE;
+    if (mode == EMU_SPLIT_FP16 && (reinterpret_cast<uintptr_t>(x) & 7u)) return EMU_STATUS_NOT_SUPPORTED;
+    int dev = 0, sms = 0;
+    emu_status st = device_check(dev, sms);
+    if (st != EMU_STATUS_SUCCESS) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)std::max(1, sms * 8);
+    if (mode == EMU_SPLIT_FP16)
+        split_fp16_kernel<<<grid, 256, 0, s>>>(x, count, static_cast<uint16_t*>(hi), static_cast<uint16_t*>(lo));
+    else
+        split_tf32_kernel<<<grid, 256, 0, s>>>(x, count, static_cast<uint32_t*>(hi), static_cast<uint32_t*>(lo));
+    g_last_launches = 1;
+    return launch_status(cudaGetLastError());
+}
+
+__attribute__((visibility("default"))) emu_status emu_sgemm_batched_host(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
+                                  const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
+                                  long long strideC, int batch, emu_split_mode mode, void* stream)
+{
+    g_last_launches = 0;
+    if (m < 0 || n < 0 || k < 0 || batch < 0) return EMU_STATUS_INVALID_VALUE;
+    if (mode != EMU_SPLIT_FP16 && mode != EMU_SPLIT_TF32) return EMU_STATUS_INVALID_VALUE;
+    if (lda < std::max(1, m) || ldb < std::max(1, k) || ldc < std::max(1, m)) return EMU_STATUS_INVALID_VALUE;
+    if (strideA < 0 || strideB < 0 || strideC < 0) return EMU_STATUS_INVALID_VALUE;
+    if (m == 0 || n == 0 || batch == 0) return EMU_STATUS_SUCCESS;
+    if (C == nullptr) return EMU_STATUS_INVALID_VALUE;
+    if (batch > 1 && strideC < (long long)ldc * n) return EMU_STATUS_INVALID_VALUE;
+    const bool reads_ab = k > 0 && alpha != 0.0f;
+    if (reads_ab && (A == nullptr || B == nullptr)) return EMU_STATUS_INVALID_VALUE;
+    int dev = 0, sms = 0;
+    emu_status st = device_check(dev, sms);
+    if (st != EMU_STATUS_SUCCESS) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+    // device buffers mirror the host layout of one chunk of problems; only the
+    // m x k / k x n / m x n parts are copied (2-D copies), gaps are left alone
+    auto span = [](long long ld, long long cols, long long rows, long long stride, int nb) {
+        return (long long)(nb - 1) * stride + ld * (cols - 1) + rows;
+    };
+    auto copy = [&](float* dst, const float* src, long long ld, long long cols, long long rows, long long stride,
+                    int nb, cudaMemcpyKind kind) -> bool {
+        if (nb == 1 || stride == ld * cols) {
+            const long long h = (nb == 1 ? 1 : nb) * cols;
+            return cudaMemcpy2DAsync(dst, ld * 4, src, ld * 4, rows * 4, h, kind, s) == cudaSuccess;
+        }
+        for (int i = 0; i < nb; ++i)
+            if (cudaMemcpy2DAsync(dst + i * stride, ld * 4, src + i * stride, ld * 4, rows * 4, cols, kind, s) !=
+                cudaSuccess)
+                return false;
+        return true;
+    };
+    const int per = batch;
+    const long long spanA = reads_ab ? span(lda, k, m, strideA, per) : 0;
+    const long long spanB = reads_ab ? span(ldb, n, k, strideB, per) : 0;
+    const long long spanC = span(ldc, n, m, strideC, per);
+    float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    if (reads_ab) {
+        if (cudaMallocAsync((void**)&dA, sizeof(float) * spanA, s) != cudaSuccess) return EMU_STATUS_CUDA_ERROR;
+        if (cudaMallocAsync((void**)&dB, sizeof(float) * spanB, s) != cudaSuccess) {
+            cudaFreeAsync(dA, s);
+            return EMU_STATUS_CUDA_ERROR;
+        }
+    }
+    if (cudaMallocAsync((void**)&dC, sizeof(float) * spanC, s) != cudaSuccess) {
+        if (dA) cudaFreeAsync(dA, s);
+        if (dB) cudaFreeAsync(dB, s);
+        return EMU_STATUS_CUDA_ERROR;
+    }
+    int launches = 0;
+    bool ok = true;
+    if (reads_ab) {
+        ok = ok && copy(dA, A, lda, k, m, strideA, strideA == 0 ? 1 : batch, cudaMemcpyHostToDevice);
+        ok = ok && copy(dB, B, ldb, n, k, strideB, strideB == 0 ? 1 : batch, cudaMemcpyHostToDevice);
+    }
+    if (beta != 0.0f) ok = ok && copy(dC, C, ldc, n, m, strideC, batch, cudaMemcpyHostToDevice);
+    if (!ok) st = EMU_STATUS_CUDA_ERROR;
+    if (st == EMU_STATUS_SUCCESS) {
+        st = emu_sgemm_batched_ex(m, n, k, alpha, dA, lda, strideA, dB, ldb, strideB, beta, dC, ldc, strideC, batch,
+                                  mode, stream, nullptr, 0, 0u);
+        launches += g_last_launches;
+    }
+    if (st == EMU_STATUS_SUCCESS && !copy(C, dC, ldc, n, m, strideC, batch, cudaMemcpyDeviceToHost))
+        st = EMU_STATUS_CUDA_ERROR;
+    if (dA) cudaFreeAsync(dA, s);
+    if (dB) cudaFreeAsync(dB, s);
+    cudaFreeAsync(dC, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess && st == EMU_STATUS_SUCCESS) st = EMU_STATUS_CUDA_ERROR;
+    g_last_launches = launches;
+    return st;
+}
+
+}  // extern "C"

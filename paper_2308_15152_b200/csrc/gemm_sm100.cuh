@@ -1,0 +1,377 @@
+// gemm_sm100.cuh -- the emulated-SGEMM kernel for B200 (sm_100a).
+//
+// One persistent CTA per SM walks output tiles (batch, m-tile, n-tile) of
+// BM x BN = 128 x BN.  Warp roles (16 warps):
+//   warp 0      TMA producer: FP32 tiles of A (128 m x 32 k) and B (32 k x BN n)
+//               HBM -> shared memory ring `f32` (S32 stages), mbarrier complete_tx.
+//   warp 1      MMA issuer (one elected thread) + TMEM owner: per 16-k (FP16) or
+//               8-k (TF32) step three tcgen05.mma, P1 = A_hi B_hi -> D_hi,
+//               P2 = A_lo B_hi and P3 = A_hi B_lo -> D_corr (Eq. corr-5).
+//   warps 4-7   splitters: FP32 stage -> hi/lo operand tiles (Eqs. corr-1..4,
+//               P:479-488) written straight into the UMMA canonical layouts of
+//               the operand ring `op` (SOP stages).  This is the B200 form of the
+//               paper's split-on-load: the FP32 tile is read once
+//               from shared memory and each part is written once, in the layout
+//               the tensor core reads -- no separate FP16 staging copy and no
+//               re-layout pass.
+//   warps 8-15  combine/epilogue: every k-block of KB elements, tcgen05.ld of
+//               D_hi and D_corr, t = RN(D_hi + D_corr * 2^-11), C += t in FP32 RN
+//               on CUDA cores (the outside-of-TC accumulation of P:495, R#7/R#8);
+//               at the tile's end C = RN(alpha*C + RN(beta*C_old)), coalesced
+//               column-major stores.
+// TMEM: two accumulator buffers x (D_hi, D_corr) x BN columns = 512 columns, so
+// the MMA warp fills one buffer while the combine warps drain the other.
+//
+// Shared-memory layouts (all buffers 1024-byte aligned):
+//   f32 A  [32 k][128 m] fp32, plain (TMA box {128, 32}); 512-byte rows
+//   f32 B  [BN n][32 k]  fp32, TMA SWIZZLE_128B (box {32, BN}); 128-byte rows
+//   op A_hi/A_lo  MN-major SWIZZLE_128B canonical layout:
+//                 [k/8][m/(128B/esz)][k%8][128 B]; LBO = 1024 (next MN block),
+//                 SBO = (BM*esz/128)*1024 (next 8-k group)
+//   op B_hi/B_lo  K-major, one row of 32 k per n: FP16 64-byte rows SWIZZLE_64B
+//                 (SBO 512), TF32 128-byte rows SWIZZLE_128B (SBO 1024)
+// Swizzles are XORs on absolute shared addresses: 16-byte chunk bits [4,7)
+// (SW128) or [4,6) (SW64) ^= bits [7,10) / [7,9), which is what both TMA and
+// the UMMA descriptor apply.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+
+#include "sm100_ptx.cuh"
+#include "split.cuh"
+
+namespace emu {
+
+struct GemmParams {
+    int m, n, k;
+    int a_batched, b_batched;     // 0: batch coordinate 0 for every problem (stride 0)
+    float alpha, beta;
+    float* C;
+    long long ldc, strideC;
+    int tiles_m, tiles_n;
+    long long num_tiles;
+    int num_k_stages;             // ceil(k / 32)
+    int kb_stages;                // KB / 32
+    int corr;                     // 1 = the paper's method; 0 = "correction off" control
+    unsigned int* range_flag;     // nullable (FP16 mode only)
+};
+
+template <int MODE, int BN>
+struct GemmCfg {
+    static constexpr int BM = 128;
+    static constexpr int BK = 32;                       // k per FP32 stage
+    static constexpr int ESZ = MODE == 0 ? 2 : 4;       // operand bytes per element
+    static constexpr int KSTEP = MODE == 0 ? 16 : 8;    // UMMA K per instruction
+    static constexpr int NSTEPS = BK / KSTEP;           // MMAs per product per stage
+    static constexpr uint32_t A32_BYTES = BK * BM * 4;
+    static constexpr uint32_t B32_BYTES = BK * BN * 4;
+    static constexpr uint32_t F32_STAGE = A32_BYTES + B32_BYTES;
+    static constexpr uint32_t AOP_BYTES = BM * BK * ESZ;
+    static constexpr uint32_t BOP_BYTES = BN * BK * ESZ;
+    static constexpr uint32_t OP_STAGE = 2 * AOP_BYTES + 2 * BOP_BYTES;
+    static constexpr int S32 = MODE == 0 ? 3 : 2;
+    static constexpr int SOP = MODE == 0 ? 3 : 2;
+    static constexpr uint32_t A_MNBLK = 128 / ESZ;      // MN elements per 128-byte row
+    static constexpr uint32_t A_SBO = (BM / A_MNBLK) * 1024;
+    static constexpr uint32_t B_ROW = BK * ESZ;         // 64 (FP16) or 128 (TF32)
+    static constexpr uint32_t B_SBO = 8 * B_ROW;
+    static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;  // SW64 / SW128
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
+    static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + BAR_BYTES;
+    static constexpr int NUM_THREADS = 512;
+    static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 4;
+    static constexpr int EPI_WARP0 = 8, NUM_EPI_WARPS = 8;
+    static_assert(2 * 2 * BN <= 512, "two (D_hi, D_corr) buffers must fit TMEM");
+    static_assert(SMEM_BYTES <= 232448, "shared memory");
+};
+
+// tile index -> (batch, m-tile, n-tile); groups of up to 16 m-tiles walk the
+// n-tiles together so that concurrently running CTAs share A and B in L2.
+__device__ __forceinline__ void tile_coords(const GemmParams& p, long long t, int& b, int& mt, int& nt)
+{
+    const long long per_batch = (long long)p.tiles_m * p.tiles_n;
+    b = (int)(t / per_batch);
+    int r = (int)(t - (long long)b * per_batch);
+    const int GM = p.tiles_m < 16 ? p.tiles_m : 16;
+    const int group = r / (GM * p.tiles_n);
+    const int first_m = group * GM;
+    const int gm = (p.tiles_m - first_m) < GM ? (p.tiles_m - first_m) : GM;
+    const int rr = r - group * GM * p.tiles_n;
+    mt = first_m + rr % gm;
+    nt = rr / gm;
+}
+
+template <int MODE, int BN>
+__global__ void __launch_bounds__(512, 1)
+emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const GemmParams p)
+{
+    using Cfg = GemmCfg<MODE, BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* f32buf = smem;
+    uint8_t* opbuf = smem + Cfg::S32 * Cfg::F32_STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(opbuf + Cfg::SOP * Cfg::OP_STAGE);
+    uint64_t* f32_full = bars;
+    uint64_t* f32_empty = f32_full + Cfg::S32;
+    uint64_t* op_full = f32_empty + Cfg::S32;
+    uint64_t* op_empty = op_full + Cfg::SOP;
+    uint64_t* acc_full = op_empty + Cfg::SOP;
+    uint64_t* acc_empty = acc_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const uint32_t warp = ptx::warp_id();
+    const uint32_t lane = ptx::lane_id();
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < Cfg::S32; ++i) {
+            ptx::mbar_init(&f32_full[i], 1);
+            ptx::mbar_init(&f32_empty[i], Cfg::NUM_SPLIT_WARPS * 32);
+        }
+        for (int i = 0; i < Cfg::SOP; ++i) {
+            ptx::mbar_init(&op_full[i], Cfg::NUM_SPLIT_WARPS * 32);
+            ptx::mbar_init(&op_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&acc_full[i], 1);
+            ptx::mbar_init(&acc_empty[i], Cfg::NUM_EPI_WARPS * 32);
+        }
+        ptx::fence_mbar_init();
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int nks = p.num_k_stages;
+    const int nkb = (nks + p.kb_stages - 1) / p.kb_stages;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (ptx::elect_one()) {
+            const uint64_t pol_a = ptx::l2_policy_evict_last();
+            const uint64_t pol_b = ptx::l2_policy_evict_last();
+            uint32_t s = 0, ph = 0;
+            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                int b, mt, nt;
+                tile_coords(p, t, b, mt, nt);
+                const int ab = p.a_batched ? b : 0, bb = p.b_batched ? b : 0;
+                for (int ks = 0; ks < nks; ++ks) {
+                    ptx::mbar_wait(&f32_empty[s], ph ^ 1);
+                    uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
+                    ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
+                    ptx::tma_load_3d(dst, &tmA, &f32_full[s], mt * Cfg::BM, ks * Cfg::BK, ab, pol_a);
+                    ptx::tma_load_3d(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK, nt * BN, bb, pol_b);
+                    if (++s == Cfg::S32) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (ptx::elect_one()) {
+            constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 1u, 0u, Cfg::BM, BN);
+            uint32_t s = 0, ph = 0, acc_it = 0;
+            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                    const uint32_t buf = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+                    ptx::mbar_wait(&acc_empty[buf], aph ^ 1);
+                    ptx::tc_fence_after();
+                    const uint32_t d_hi = tmem_base + buf * 2 * BN;
+                    const uint32_t d_corr = d_hi + BN;
+                    const int ks0 = kb * p.kb_stages;
+                    const int ks1 = min(ks0 + p.kb_stages, nks);
+                    for (int ks = ks0; ks < ks1; ++ks) {
+                        ptx::mbar_wait(&op_full[s], ph);
+                        ptx::tc_fence_after();
+                        const uint32_t base = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+                        const uint32_t a_hi = base, a_lo = base + Cfg::AOP_BYTES;
+                        const uint32_t b_hi = base + 2 * Cfg::AOP_BYTES;
+                        const uint32_t b_lo = b_hi + Cfg::BOP_BYTES;
+#pragma unroll
+                        for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                            // A: MN-major SW128, one K step = KSTEP/8 k-groups of SBO bytes
+                            const uint32_t aoff = st * (Cfg::KSTEP / 8) * Cfg::A_SBO;
+                            // B: K-major, one K step = 32 bytes along the swizzled row
+                            const uint32_t boff = st * 32;
+                            const uint64_t dA_hi = ptx::smem_desc(a_hi + aoff, 1024, Cfg::A_SBO, 2);
+                            const uint64_t dA_lo = ptx::smem_desc(a_lo + aoff, 1024, Cfg::A_SBO, 2);
+                            const uint64_t dB_hi = ptx::smem_desc(b_hi + boff, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                            const uint64_t dB_lo = ptx::smem_desc(b_lo + boff, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                            const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                            if (MODE == 0) {
+                                ptx::mma_f16(d_hi, dA_hi, dB_hi, idesc, acc);            // P1
+                                if (p.corr) {
+                                    ptx::mma_f16(d_corr, dA_lo, dB_hi, idesc, acc);      // P2
+                                    ptx::mma_f16(d_corr, dA_hi, dB_lo, idesc, 1u);       // P3
+                                }
+                            } else {
+                                ptx::mma_tf32(d_hi, dA_hi, dB_hi, idesc, acc);
+                                if (p.corr) {
+                                    ptx::mma_tf32(d_corr, dA_lo, dB_hi, idesc, acc);
+                                    ptx::mma_tf32(d_corr, dA_hi, dB_lo, idesc, 1u);
+                                }
+                            }
+                        }
+                        ptx::tc_commit(&op_empty[s]);   // operand stage free when these MMAs finish
+                        if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                    }
+                    ptx::tc_commit(&acc_full[buf]);     // k-block accumulators ready
+                }
+            }
+        }
+    } else if (warp >= Cfg::SPLIT_WARP0 && warp < Cfg::SPLIT_WARP0 + Cfg::NUM_SPLIT_WARPS) {
+        // ------------------------------------------------ splitters
+        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;   // 0..127
+        const uint32_t sw = tid >> 5;
+        uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
+        uint32_t nonfinite = 0;
+        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int ks = 0; ks < nks; ++ks) {
+                ptx::mbar_wait(&f32_full[s32], ph32);
+                ptx::mbar_wait(&op_empty[sop], phop ^ 1);
+                const uint8_t* fa = f32buf + s32 * Cfg::F32_STAGE;
+                const uint8_t* fb = fa + Cfg::A32_BYTES;
+                uint8_t* o = opbuf + sop * Cfg::OP_STAGE;
+                uint8_t* oa_hi = o;
+                uint8_t* oa_lo = o + Cfg::AOP_BYTES;
+                uint8_t* ob_hi = o + 2 * Cfg::AOP_BYTES;
+                uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
+                // A: warp sw handles k rows sw, sw+4, ...; lane handles m = 4*lane .. +3
+#pragma unroll
+                for (int kk = 0; kk < Cfg::BK / 4; ++kk) {
+                    const uint32_t k = sw + 4 * kk;
+                    const float4 v = *reinterpret_cast<const float4*>(fa + k * 512 + lane * 16);
+                    const uint32_t g = k >> 3, kr = k & 7;
+                    if (MODE == 0) {
+                        uint32_t h01, l01, h23, l23;
+                        split_fp16x2(v.x, v.y, h01, l01);
+                        split_fp16x2(v.z, v.w, h23, l23);
+                        nonfinite |= f16x2_nonfinite(h01) | f16x2_nonfinite(h23);
+                        const uint32_t mblk = lane >> 4, chunk = (lane & 15) >> 1;
+                        const uint32_t off = g * Cfg::A_SBO + mblk * 1024 + kr * 128 + ((chunk ^ kr) << 4) + (lane & 1) * 8;
+                        *reinterpret_cast<uint2*>(oa_hi + off) = make_uint2(h01, h23);
+                        *reinterpret_cast<uint2*>(oa_lo + off) = make_uint2(l01, l23);
+                    } else {
+                        uint4 h, l;
+                        split_tf32(v.x, h.x, l.x);
+                        split_tf32(v.y, h.y, l.y);
+                        split_tf32(v.z, h.z, l.z);
+                        split_tf32(v.w, h.w, l.w);
+                        const uint32_t mblk = lane >> 3, chunk = lane & 7;
+                        const uint32_t off = g * Cfg::A_SBO + mblk * 1024 + kr * 128 + ((chunk ^ kr) << 4);
+                        *reinterpret_cast<uint4*>(oa_hi + off) = h;
+                        *reinterpret_cast<uint4*>(oa_lo + off) = l;
+                    }
+                }
+                // B: one n row (32 k) per thread
+#pragma unroll
+                for (int rr = 0; rr < BN / 128; ++rr) {
+                    const uint32_t n = tid + rr * 128;
+                    const uint8_t* row = fb + n * 128;
+                    if (MODE == 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {   // 8 k per 16-byte FP16 chunk
+                            const float4 v0 = *reinterpret_cast<const float4*>(row + (((2 * j) ^ (n & 7)) << 4));
+                            const float4 v1 = *reinterpret_cast<const float4*>(row + (((2 * j + 1) ^ (n & 7)) << 4));
+                            uint4 h, l;
+                            split_fp16x2(v0.x, v0.y, h.x, l.x);
+                            split_fp16x2(v0.z, v0.w, h.y, l.y);
+                            split_fp16x2(v1.x, v1.y, h.z, l.z);
+                            split_fp16x2(v1.z, v1.w, h.w, l.w);
+                            nonfinite |= f16x2_nonfinite(h.x) | f16x2_nonfinite(h.y) |
+                                         f16x2_nonfinite(h.z) | f16x2_nonfinite(h.w);
+                            const uint32_t off = n * 64 + ((j ^ ((n >> 1) & 3)) << 4);
+                            *reinterpret_cast<uint4*>(ob_hi + off) = h;
+                            *reinterpret_cast<uint4*>(ob_lo + off) = l;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {   // 4 k per 16-byte TF32 chunk
+                            const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (n & 7)) << 4));
+                            uint4 h, l;
+                            split_tf32(v.x, h.x, l.x);
+                            split_tf32(v.y, h.y, l.y);
+                            split_tf32(v.z, h.z, l.z);
+                            split_tf32(v.w, h.w, l.w);
+                            const uint32_t off = n * 128 + ((j ^ (n & 7)) << 4);
+                            *reinterpret_cast<uint4*>(ob_hi + off) = h;
+                            *reinterpret_cast<uint4*>(ob_lo + off) = l;
+                        }
+                    }
+                }
+                ptx::fence_proxy_async_smem();        // our st.shared -> visible to UMMA
+                ptx::mbar_arrive(&op_full[sop]);
+                ptx::mbar_arrive(&f32_empty[s32]);
+                if (++s32 == Cfg::S32) { s32 = 0; ph32 ^= 1; }
+                if (++sop == Cfg::SOP) { sop = 0; phop ^= 1; }
+            }
+        }
+        if (MODE == 0 && p.range_flag != nullptr) {
+            nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+            if (nonfinite && lane == 0) atomicOr(p.range_flag, 1u);
+        }
+    } else if (warp >= Cfg::EPI_WARP0) {
+        // ------------------------------------------------ combine + epilogue
+        constexpr int HALF = BN / 2;
+        const uint32_t e = warp - Cfg::EPI_WARP0;
+        const uint32_t q = warp & 3;            // TMEM lane quadrant this warp may access
+        const uint32_t h = e >> 2;              // column half
+        const float scale = MODE == 0 ? (1.0f / 2048.0f) : 1.0f;
+        uint32_t acc_it = 0;
+        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            int b, mt, nt;
+            tile_coords(p, t, b, mt, nt);
+            float creg[HALF];
+#pragma unroll
+            for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
+            for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                const uint32_t buf = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+                ptx::mbar_wait(&acc_full[buf], aph);
+                ptx::tc_fence_after();
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * BN + h * HALF;
+#pragma unroll
+                for (int c = 0; c < HALF / 16; ++c) {
+                    float vh[16], vc[16];
+                    ptx::tmem_ld16(taddr + c * 16, vh);
+                    ptx::tmem_ld16(taddr + BN + c * 16, vc);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float tt = p.corr ? fmaf(vc[j], scale, vh[j]) : vh[j];
+                        creg[c * 16 + j] = __fadd_rn(creg[c * 16 + j], tt);
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&acc_empty[buf]);
+            }
+            // epilogue: C = RN(alpha*C + RN(beta*C_old)), column-major, coalesced per column
+            const int row = mt * Cfg::BM + (int)(q * 32 + lane);
+            const int col0 = nt * BN + (int)(h * HALF);
+            if (row < p.m) {
+                float* cp = p.C + (long long)b * p.strideC + row + (long long)col0 * p.ldc;
+#pragma unroll
+                for (int j = 0; j < HALF; ++j) {
+                    if (col0 + j < p.n) {
+                        float* dst = cp + (long long)j * p.ldc;
+                        const float bc = p.beta != 0.0f ? __fmul_rn(p.beta, *dst) : 0.0f;
+                        *dst = fmaf(p.alpha, creg[j], bc);
+                    }
+                }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace emu

@@ -1,0 +1,68 @@
+// split.cuh -- the operand split of Eqs. corr-1..corr-4
+// and its TF32 variant (R#6), as register-level device functions.
+// The same functions run inside the GEMM's splitter warps and in the
+// emu_split export, so the bit-exact split test covers the GEMM's staging.
+//
+// FP16: hi = toFP16(x) (RNE, IEEE subnormals, overflow -> Inf: R#1, R#3, R#4)
+//       lo = toFP16((x - toFP32(hi)) * 2^11)
+//   cvt.rn.f16x2.f32 does both roundings; x - hi and the 2^11 scaling use the
+//   _rn intrinsics so they can never be contracted into an FMA.
+// TF32: hi = RNE_tf32(x), lo = RNE_tf32(x - hi), with the low 13 bits cleared
+//   explicitly so the tensor core's treatment of them is irrelevant (R#6).
+#pragma once
+
+#include <cstdint>
+
+namespace emu {
+
+// two floats -> packed binary16 pair, element x0 in the low half
+__device__ __forceinline__ uint32_t f32x2_to_f16x2_rn(float x0, float x1)
+{
+    uint32_t h;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+    return h;
+}
+
+__device__ __forceinline__ void f16x2_to_f32x2(uint32_t h, float& x0, float& x1)
+{
+    asm("{\n\t.reg .f16 a, b;\n\t"
+        "mov.b32 {a, b}, %2;\n\t"
+        "cvt.f32.f16 %0, a;\n\t"
+        "cvt.f32.f16 %1, b;\n\t}"
+        : "=f"(x0), "=f"(x1) : "r"(h));
+}
+
+// Eqs. corr-1/corr-2 for two elements: packed hi and packed lo (low half = x0)
+__device__ __forceinline__ void split_fp16x2(float x0, float x1, uint32_t& hi, uint32_t& lo)
+{
+    hi = f32x2_to_f16x2_rn(x0, x1);
+    float h0, h1;
+    f16x2_to_f32x2(hi, h0, h1);
+    const float r0 = __fmul_rn(__fsub_rn(x0, h0), 2048.0f);
+    const float r1 = __fmul_rn(__fsub_rn(x1, h1), 2048.0f);
+    lo = f32x2_to_f16x2_rn(r0, r1);
+}
+
+// 1 if either binary16 half of `h` is +-Inf or NaN (exponent field all ones)
+__device__ __forceinline__ uint32_t f16x2_nonfinite(uint32_t h)
+{
+    const uint32_t e = h & 0x7c007c00u;
+    return ((e & 0xffffu) == 0x7c00u) | ((e >> 16) == 0x7c00u);
+}
+
+// binary32 -> TF32 (RNE at fraction bit 13); Inf stays Inf, NaN stays a quiet NaN
+__device__ __forceinline__ uint32_t tf32_rn_bits(uint32_t u)
+{
+    const uint32_t r = (u + 0xfffu + ((u >> 13) & 1u)) & 0xffffe000u;
+    const bool special = (u & 0x7f800000u) == 0x7f800000u;
+    const uint32_t s = (u & 0x7fffffu) ? ((u | 0x400000u) & 0xffffe000u) : u;
+    return special ? s : r;
+}
+
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo)
+{
+    hi = tf32_rn_bits(__float_as_uint(x));
+    lo = tf32_rn_bits(__float_as_uint(__fsub_rn(x, __uint_as_float(hi))));
+}
+
+}  // namespace emu

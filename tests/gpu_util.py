@@ -1,0 +1,60 @@
+"""GPU-side helpers for the parity tests: run the C ABI on column-major numpy
+operands (layout of `workloads`) and compute the element-wise tolerance
+ from the oracle's |A||B|."""
+import math
+
+import numpy as np
+
+import oracle
+
+U = 2.0 ** -24
+
+
+def emu_gpu(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kblock=0, flags=0, range_flag=None,
+            ldc=None):
+    import torch
+    import paper_2308_15152_b200 as emu
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    B = np.ascontiguousarray(B, dtype=np.float32)
+    if A.ndim == 2:
+        A = A[None]
+    if B.ndim == 2:
+        B = B[None]
+    batch = max(A.shape[0], B.shape[0])
+    lda, ldb = A.shape[2], B.shape[2]
+    sA = 0 if (A.shape[0] == 1 and batch > 1) else A.shape[1] * lda
+    sB = 0 if (B.shape[0] == 1 and batch > 1) else B.shape[1] * ldb
+    ldc = m if ldc is None else ldc
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    if C is None:
+        dC = torch.full((batch, n, ldc), float("nan"), device="cuda")
+    else:
+        dC = torch.from_numpy(np.ascontiguousarray(C, dtype=np.float32).reshape(batch, n, ldc)).cuda()
+    emu.emu_sgemm_batched_ex(m, n, k, alpha, dA, lda, sA, dB, ldb, sB, beta, dC, ldc, n * ldc, batch,
+                             mode, None, range_flag, kblock, flags)
+    torch.cuda.synchronize()
+    return dC.cpu().numpy()
+
+
+def tolerance(mode, A, B, m, n, k, kblock=64):
+    """Element-wise bound on |C_gpu - C_oracle|: the tensor
+    core's own accumulation of each k-block (at most 2 binary32 ulps per MMA
+    instruction of K_inst products plus the block's final alignment), and one
+    ulp per cross-block add of the two differently-rounded running sums:
+        gamma = 2*(KB/K_inst) + 4 + 2*ceil(k/KB),  tol = gamma * u * (|A||B|)_ij
+    """
+    kb = kblock or 64
+    kinst = 16 if mode in (0, "fp16") else 8
+    gamma = 2 * (kb / kinst) + 4 + 2 * math.ceil(max(k, 1) / kb)
+    A = np.asarray(A)
+    B = np.asarray(B)
+    if A.ndim == 2:
+        A = A[None]
+    if B.ndim == 2:
+        B = B[None]
+    batch = max(A.shape[0], B.shape[0])
+    out = np.empty((batch, n, m))
+    for b in range(batch):
+        out[b] = oracle.absgemm_f64(A[b if A.shape[0] > 1 else 0], B[b if B.shape[0] > 1 else 0], m, n, k)
+    return gamma * U * out

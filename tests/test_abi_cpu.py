@@ -1,0 +1,98 @@
+"""The C-ABI library loads, exports every symbol include/emu_sgemm.h declares,
+and its host-side validation (which runs before any CUDA call) behaves as the
+header documents.  No compute calls: no GPU here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "emu_sgemm.h")
+
+
+@pytest.fixture(scope="module")
+def emu():
+    from paper_2308_15152_b200 import build
+    build.build()
+    import paper_2308_15152_b200 as emu
+    return emu
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(emu_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for required in ["emu_sgemm", "emu_sgemm_batched", "emu_sgemm_batched_ex", "emu_split",
+                     "emu_status_string", "emu_version", "emu_sgemm_batched_host"]:
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(emu):
+    lib = ctypes.CDLL(emu.LIB_PATH)
+    for name in _declared():
+        assert hasattr(lib, name), name
+
+
+def test_only_declared_symbols_are_exported(emu):
+    out = os.popen(f"nm -D --defined-only {emu.LIB_PATH}").read()
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l and l.split()[-1].startswith("emu_")}
+    assert exported == set(_declared())
+
+
+def test_library_is_sm100a_only(emu):
+    out = os.popen(f"cuobjdump --list-elf {emu.LIB_PATH}").read()
+    assert "sm_100a" in out
+    assert all("sm_100a" in l for l in out.splitlines() if l.strip())
+
+
+def test_status_strings_and_version(emu):
+    for s in range(6):
+        assert emu.emu_status_string(s).startswith("EMU_STATUS_")
+    assert emu.emu_status_string(99) == "EMU_STATUS_UNKNOWN"
+    assert emu.emu_version() >= 100
+
+
+def _call(emu, **kw):
+    a = dict(m=8, n=8, k=8, alpha=1.0, A=16, lda=8, strideA=0, B=16, ldb=8, strideB=0, beta=0.0,
+             C=16, ldc=8, strideC=64, batch=1, mode=0)
+    a.update(kw)
+    return emu.lib.emu_sgemm_batched(a["m"], a["n"], a["k"], a["alpha"], a["A"], a["lda"], a["strideA"],
+                                     a["B"], a["ldb"], a["strideB"], a["beta"], a["C"], a["ldc"],
+                                     a["strideC"], a["batch"], a["mode"], None)
+
+
+@pytest.mark.parametrize("kw", [dict(m=-1), dict(n=-1), dict(k=-1), dict(batch=-1), dict(mode=2),
+                                dict(lda=7), dict(ldb=7), dict(ldc=7), dict(C=None),
+                                dict(A=None), dict(B=None), dict(strideA=-4),
+                                dict(batch=2, strideC=63)])
+def test_invalid_arguments_rejected_before_launch(emu, kw):
+    assert _call(emu, **kw) == 1   # EMU_STATUS_INVALID_VALUE
+
+
+@pytest.mark.parametrize("kw", [dict(m=0), dict(n=0), dict(batch=0), dict(m=0, C=None)])
+def test_quick_return_without_device(emu, kw):
+    assert _call(emu, **kw) == 0
+    assert emu.emu_last_launch_count() == 0
+
+
+def test_ex_validation(emu):
+    L = emu.lib
+    args = [8, 8, 8, 1.0, 16, 8, 0, 16, 8, 0, 0.0, 16, 8, 0, 1, 0, None, None]
+    assert L.emu_sgemm_batched_ex(*args, 48, 0) == 1      # kblock not a multiple of 32
+    assert L.emu_sgemm_batched_ex(*args, -32, 0) == 1
+    assert L.emu_sgemm_batched_ex(*args, 8192, 0) == 1
+    assert L.emu_sgemm_batched_ex(*args, 0, 4) == 1       # unknown flag bit
+
+
+def test_split_validation(emu):
+    L = emu.lib
+    assert L.emu_split(16, -1, 0, 16, 16, None) == 1
+    assert L.emu_split(16, 4, 7, 16, 16, None) == 1
+    assert L.emu_split(None, 4, 0, 16, 16, None) == 1
+    assert L.emu_split(18, 4, 0, 16, 16, None) == 1       # misaligned
+    assert L.emu_split(None, 0, 0, None, None, None) == 0

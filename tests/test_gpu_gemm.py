@@ -1,0 +1,264 @@
+"""GPU parity of the emulated SGEMM (C ABI -> sm_100a tcgen05 kernels) against
+the CPU oracle, element by element on the same seeded inputs.
+
+Bars:
+  * bit-exact where the method's result is exact: identity / permutation
+    operands (C == reconstruct(split(B))), small-integer operands (exact
+    integer product), quick returns;
+  * elsewhere |C_gpu - C_oracle| <= gamma u (|A||B|)_ij (tests/gpu_util.py),
+    the tensor core's in-block accumulation being the only freedom;
+  * north_star's accuracy gate vs FP64: rel-Frobenius <= 2x plain FP32 SGEMM
+    and <= 1e-5 for k <= 4096, uniform[-1,1].
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from gpu_util import emu_gpu, tolerance
+
+pytestmark = pytest.mark.gpu
+MODES = ["fp16", "tf32"]
+
+
+def _cmp(mode, A, B, m, n, k, kblock=0, **kw):
+    C = emu_gpu(mode, A, B, m, n, k, kblock=kblock, **kw)
+    kb = kblock or 64
+    ref = oracle.emu_gemm(mode, A, B, m, n, k, kb=kb, alpha=kw.get("alpha", 1.0),
+                          beta=kw.get("beta", 0.0), C=kw.get("C"),
+                          corr=not (kw.get("flags", 0) & 1))
+    tol = tolerance(mode, A, B, m, n, k, kb)
+    if kw.get("beta", 0.0) != 0.0:
+        tol = tol + 2.0 ** -23 * np.abs(np.asarray(kw["C"], dtype=np.float64)).reshape(tol.shape)
+    d = np.abs(C[..., :m].astype(np.float64) - ref[..., :m].astype(np.float64))
+    ratio = np.max(d / np.where(tol > 0, tol, 1.0))
+    assert np.all(d <= tol), f"max |gpu-oracle|/tol = {ratio:.3g}"
+    return C, ref
+
+
+# ------------------------------------------------------------- exactness ----
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("kblock", [0, 32, 128])
+def test_identity_and_permutation_bit_exact(mode, kblock):
+    m = n = k = 160   # two m-tiles, two n-tiles, 5 k-stages (ragged tiles)
+    _, B = workloads.make_operands(1, m, n, k, seed=21)
+    perm = workloads.rng(4).permutation(k)
+    for P in (np.eye(k, dtype=np.float32), np.eye(k, dtype=np.float32)[perm]):
+        A = workloads.colmajor(P)[None]
+        C = emu_gpu(mode, A, B, m, n, k, kblock=kblock)
+        ref = oracle.emu_gemm(mode, A, B, m, n, k, kb=kblock or 64)
+        assert np.array_equal(C, ref)
+        # B = P: C == reconstruct(split(A))
+        C2 = emu_gpu(mode, B, workloads.colmajor(P)[None], m, n, k, kblock=kblock)
+        ref2 = oracle.emu_gemm(mode, B, workloads.colmajor(P)[None], m, n, k, kb=kblock or 64)
+        assert np.array_equal(C2, ref2)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("shape", [(37, 29, 300, 3), (128, 128, 32, 1), (1, 1, 1, 1),
+                                   (300, 260, 1000, 2), (129, 257, 33, 1)])
+def test_small_integers_exact(mode, shape):
+    m, n, k, batch = shape
+    A, B = workloads.make_operands(batch, m, n, k, seed=8, dist="int16")
+    C0 = workloads.small_int((batch, n, m), seed=9)
+    exact = oracle.emu_gemm(mode, A, B, m, n, k)
+    assert np.array_equal(emu_gpu(mode, A, B, m, n, k), exact)
+    exact1 = oracle.emu_gemm(mode, A, B, m, n, k, beta=1.0, C=C0)
+    assert np.array_equal(emu_gpu(mode, A, B, m, n, k, beta=1.0, C=C0), exact1)
+
+
+# ---------------------------------------------------------------- parity ----
+SHAPES = [
+    (16, 64, 64, 64),        # c1 (BASELINE.json configs[0])
+    (2, 200, 136, 300),      # ragged m, n, k over several tiles and k-blocks
+    (1, 128, 128, 32),       # exactly one tile, one stage
+    (1, 129, 257, 33),       # one past every tile edge
+    (4, 256, 256, 256),      # c2 item shape
+    (1, 64, 384, 1000),
+    (1, 4, 4, 4096),         # long k, tiny tile
+]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_parity_uniform(mode, shape):
+    batch, m, n, k = shape
+    A, B = workloads.make_operands(batch, m, n, k, seed=100 + m + k)
+    _cmp(mode, A, B, m, n, k)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("kblock", [32, 64, 256, 4096])
+def test_parity_kblock(mode, kblock):
+    m, n, k = 128, 128, 1024
+    A, B = workloads.make_operands(1, m, n, k, seed=77)
+    _cmp(mode, A, B, m, n, k, kblock=kblock)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_wide_magnitudes(mode):
+    m, n, k = 96, 160, 512
+    A, B = workloads.make_operands(1, m, n, k, seed=78, dist="logu15")
+    _cmp(mode, A, B, m, n, k)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_alpha_beta(mode):
+    m, n, k, batch = 150, 140, 130, 3
+    A, B = workloads.make_operands(batch, m, n, k, seed=5)
+    C0 = workloads.uniform((batch, n, m), seed=6)
+    _cmp(mode, A, B, m, n, k, alpha=-1.5, beta=0.75, C=C0)
+    # beta == 0 never reads C (NaN-filled C in emu_gpu)
+    C = emu_gpu(mode, A, B, m, n, k, alpha=1.0, beta=0.0)
+    assert np.all(np.isfinite(C))
+    # alpha == 0 / k == 0 quick returns: C = RN(beta*C), bit-exact
+    out = emu_gpu(mode, A, B, m, n, k, alpha=0.0, beta=0.5, C=C0)
+    assert np.array_equal(out, (C0 * np.float32(0.5)).reshape(out.shape))
+    out = emu_gpu(mode, A, B, m, n, 0, alpha=1.0, beta=0.0, C=C0)
+    assert np.array_equal(out, np.zeros_like(out))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_leading_dimensions_and_broadcast(mode):
+    m, n, k, batch = 100, 70, 90, 3
+    A, B = workloads.make_operands(batch, m, n, k, seed=12, lda=104, ldb=96)
+    _cmp(mode, A, B, m, n, k)
+    # strideA = 0: one A shared by all problems
+    _cmp(mode, A[:1], B, m, n, k)
+    _cmp(mode, A, B[:1], m, n, k)
+    # ldc > m: rows between m and ldc untouched
+    C0 = np.full((batch, n, m + 5), 7.0, dtype=np.float32)
+    C = emu_gpu(mode, A, B, m, n, k, C=C0, ldc=m + 5)
+    assert np.all(C[..., m:] == 7.0)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_correction_off_policy(mode):
+    """EMU_FLAG_NO_CORRECTION matches the oracle's corr=False and is
+    >= 32x less accurate than the method."""
+    m = n = 128
+    k = 256
+    A, B = workloads.make_operands(1, m, n, k, seed=41)
+    Coff, _ = _cmp(mode, A, B, m, n, k, flags=1)
+    Con = emu_gpu(mode, A, B, m, n, k)
+    R = oracle.gemm_f64(A, B, m, n, k)
+    assert oracle.rel_frobenius(Coff, R) >= 32 * oracle.rel_frobenius(Con, R)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_deterministic(mode):
+    m, n, k, batch = 256, 256, 512, 4
+    A, B = workloads.make_operands(batch, m, n, k, seed=3)
+    C1 = emu_gpu(mode, A, B, m, n, k)
+    C2 = emu_gpu(mode, A, B, m, n, k)
+    assert np.array_equal(C1, C2)
+    # batch-sharded halves == the whole (the multi-GPU partition, R#20)
+    Ch = np.concatenate([emu_gpu(mode, A[:2], B[:2], m, n, k), emu_gpu(mode, A[2:], B[2:], m, n, k)])
+    assert np.array_equal(C1, Ch)
+
+
+# -------------------------------------------------------- accuracy gates ----
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("k", [64, 256, 1024, 4096])
+def test_accuracy_gate_vs_fp64(mode, k):
+    """north_star: rel-Frobenius vs FP64 <= 2x plain CPU FP32 SGEMM and <= 1e-5
+    (k <= 4096, uniform[-1,1]); P:557's claim of SGEMM-level accuracy."""
+    m = n = 128
+    for seed in (1, 2, 3):
+        A, B = workloads.make_operands(1, m, n, k, seed=seed)
+        R = oracle.gemm_f64(A, B, m, n, k)
+        e_gpu = oracle.rel_frobenius(emu_gpu(mode, A, B, m, n, k), R)
+        e_sg = oracle.rel_frobenius(oracle.sgemm_f32(A, B, m, n, k), R)
+        assert e_gpu <= 2 * e_sg and e_gpu <= 1e-5, (e_gpu, e_sg)
+
+
+def test_c4_stress_range():
+    """c4 (k = 4096, magnitudes 2^-30..2^30): FP16 mode overflows (R#4) and the
+    range flag reports it; TF32 mode passes the accuracy gate."""
+    import torch
+    m = n = 256
+    k = 4096
+    A, B = workloads.make_operands(1, m, n, k, seed=11, dist="logu30")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    C16 = emu_gpu("fp16", A, B, m, n, k, range_flag=flag)
+    assert int(flag.item()) == 1
+    assert not np.all(np.isfinite(C16))
+    R = oracle.gemm_f64(A, B, m, n, k)
+    C32 = emu_gpu("tf32", A, B, m, n, k)
+    e_sg = oracle.rel_frobenius(oracle.sgemm_f32(A, B, m, n, k), R)
+    assert oracle.rel_frobenius(C32, R) <= 2 * e_sg
+    # in range (2^-30..2^15) the FP16 mode passes too, flag stays clear
+    A, B = workloads.make_operands(1, m, n, k, seed=11, dist="logu15")
+    flag.zero_()
+    C16 = emu_gpu("fp16", A, B, m, n, k, range_flag=flag)
+    assert int(flag.item()) == 0
+    R = oracle.gemm_f64(A, B, m, n, k)
+    assert oracle.rel_frobenius(C16, R) <= 2 * oracle.rel_frobenius(oracle.sgemm_f32(A, B, m, n, k), R)
+
+
+# ---------------------------------------------- full sizes, sampled outputs ----
+def _sampled(mode, batch, m, n, k, seed, nsamp=384):
+    import torch
+    import paper_2308_15152_b200 as emu
+    A, B = workloads.make_operands(batch, m, n, k, seed=seed)
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    dC = torch.empty((batch, n, m), device="cuda")
+    emu.emu_sgemm_batched(m, n, k, 1.0, dA, m, k * m, dB, k, n * k, 0.0, dC, m, n * m, batch, mode)
+    torch.cuda.synchronize()
+    g = workloads.rng(seed + 1)
+    b = g.integers(0, batch, nsamp)
+    i = g.integers(0, m, nsamp)
+    j = g.integers(0, n, nsamp)
+    # always include the far corners of the last problem
+    b[:2], i[:2], j[:2] = batch - 1, m - 1, n - 1
+    i[1], j[1] = 0, 0
+    got = dC[torch.from_numpy(b), torch.from_numpy(j), torch.from_numpy(i)].cpu().numpy()
+    ref = oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j)
+    absab = np.array([np.dot(np.abs(A[bb, :, ii].astype(np.float64)), np.abs(B[bb, jj, :].astype(np.float64)))
+                      for bb, ii, jj in zip(b, i, j)])
+    gamma = 2 * (64 / (16 if mode == "fp16" else 8)) + 4 + 2 * math.ceil(k / 64)
+    tol = gamma * 2.0 ** -24 * absab
+    assert np.all(np.abs(got.astype(np.float64) - ref) <= tol)
+    return A, B
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c2_full_size_sampled(mode):
+    """BASELINE.json configs[1]: 1024 x 256^3 in the launch configuration
+    bench.py times; 384 sampled outputs vs the oracle."""
+    _sampled(mode, 1024, 256, 256, 256, seed=1)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c3_full_size_sampled(mode):
+    """BASELINE.json configs[2]: one 16384^3 GEMM; sampled outputs."""
+    _sampled(mode, 1, 16384, 16384, 16384, seed=7, nsamp=96)
+
+
+# ----------------------------------------------------------- host entry ----
+@pytest.mark.parametrize("mode", MODES)
+def test_host_entry_matches_device_entry(mode):
+    import paper_2308_15152_b200 as emu
+    m, n, k, batch = 100, 96, 200, 5
+    A, B = workloads.make_operands(batch, m, n, k, seed=9, lda=104)
+    C0 = workloads.uniform((batch, n, m), seed=10)
+    Ch = C0.copy()
+    emu.emu_sgemm_batched_host(m, n, k, 1.25, A, 104, k * 104, B, k, n * k, 0.5, Ch, m, n * m, batch, mode)
+    Cd = emu_gpu(mode, A, B, m, n, k, alpha=1.25, beta=0.5, C=C0)
+    assert np.array_equal(Ch, Cd)
+
+
+def test_not_supported_domain():
+    import torch
+    import paper_2308_15152_b200 as emu
+    A = torch.zeros(64 * 65, device="cuda")
+    C = torch.zeros(64 * 64, device="cuda")
+    with pytest.raises(emu.EmuError) as e:      # lda not a multiple of 4
+        emu.emu_sgemm_batched(63, 64, 64, 1.0, A, 63, 0, A, 64, 0, 0.0, C, 63, 0, 1, "fp16")
+    assert e.value.status == 2
+    with pytest.raises(emu.EmuError) as e:      # misaligned base
+        emu.emu_sgemm_batched(64, 64, 64, 1.0, A.data_ptr() + 4, 64, 0, A, 64, 0, 0.0, C, 64, 0, 1, "fp16")
+    assert e.value.status == 2
