@@ -57,7 +57,14 @@ struct GemmParams {
     unsigned int* range_flag;     // nullable (FP16 mode only)
 };
 
-template <int MODE, int BN>
+// A operand layouts in the operand ring
+enum : int {
+    A_MN_SW128 = 0,      // MN-major, SWIZZLE_128B (16-bit elements; FP16 mode)
+    A_K_SW128 = 1,       // K-major, one row of 32 k per m (TF32: 128-byte rows, SWIZZLE_128B)
+    A_MN_SW128_32B = 2,  // MN-major, SWIZZLE_128B_BASE32B (the MN-major layout for 32-bit elements)
+};
+
+template <int MODE, int BN, int ALAY = (MODE == 0 ? A_MN_SW128 : A_K_SW128)>
 struct GemmCfg {
     static constexpr int BM = 128;
     static constexpr int BK = 32;                       // k per FP32 stage
@@ -72,11 +79,19 @@ struct GemmCfg {
     static constexpr uint32_t OP_STAGE = 2 * AOP_BYTES + 2 * BOP_BYTES;
     static constexpr int S32 = MODE == 0 ? 3 : 2;
     static constexpr int SOP = MODE == 0 ? 3 : 2;
-    static constexpr uint32_t A_MNBLK = 128 / ESZ;      // MN elements per 128-byte row
-    static constexpr uint32_t A_SBO = (BM / A_MNBLK) * 1024;
     static constexpr uint32_t B_ROW = BK * ESZ;         // 64 (FP16) or 128 (TF32)
     static constexpr uint32_t B_SBO = 8 * B_ROW;
     static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;  // SW64 / SW128
+    static_assert(ALAY != A_MN_SW128 || ESZ == 2, "MN-major SW128 here is the 16-bit layout");
+    static_assert(ALAY != A_MN_SW128_32B || ESZ == 4, "BASE32B is the 32-bit MN-major layout");
+    // A descriptor: leading / stride byte offsets, layout type, bytes per K step, major
+    static constexpr uint32_t A_LBO = ALAY == A_MN_SW128 ? 1024 : ALAY == A_K_SW128 ? 16 : 512;
+    static constexpr uint32_t A_SBO = ALAY == A_MN_SW128 ? (BM / 64) * 1024
+                                    : ALAY == A_K_SW128 ? 8 * B_ROW : (BM / 32) * 512;
+    static constexpr uint32_t A_LAYOUT = ALAY == A_MN_SW128 ? 2 : ALAY == A_K_SW128 ? B_LAYOUT : 1;
+    static constexpr uint32_t A_STEP = ALAY == A_MN_SW128 ? (KSTEP / 8) * A_SBO
+                                     : ALAY == A_K_SW128 ? 32 : (KSTEP / 4) * A_SBO;
+    static constexpr uint32_t A_MAJOR = ALAY == A_K_SW128 ? 0 : 1;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
     static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + BAR_BYTES;
@@ -103,12 +118,12 @@ __device__ __forceinline__ void tile_coords(const GemmParams& p, long long t, in
     nt = rr / gm;
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, int ALAY>
 __global__ void __launch_bounds__(512, 1)
 emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const GemmParams p)
 {
-    using Cfg = GemmCfg<MODE, BN>;
+    using Cfg = GemmCfg<MODE, BN, ALAY>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* f32buf = smem;
@@ -174,7 +189,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         if (ptx::elect_one()) {
-            constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 1u, 0u, Cfg::BM, BN);
+            constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, Cfg::A_MAJOR, 0u, Cfg::BM, BN);
             uint32_t s = 0, ph = 0, acc_it = 0;
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
                 for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
@@ -194,12 +209,11 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const uint32_t b_lo = b_hi + Cfg::BOP_BYTES;
 #pragma unroll
                         for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                            // A: MN-major SW128, one K step = KSTEP/8 k-groups of SBO bytes
-                            const uint32_t aoff = st * (Cfg::KSTEP / 8) * Cfg::A_SBO;
+                            const uint32_t aoff = st * Cfg::A_STEP;
                             // B: K-major, one K step = 32 bytes along the swizzled row
                             const uint32_t boff = st * 32;
-                            const uint64_t dA_hi = ptx::smem_desc(a_hi + aoff, 1024, Cfg::A_SBO, 2);
-                            const uint64_t dA_lo = ptx::smem_desc(a_lo + aoff, 1024, Cfg::A_SBO, 2);
+                            const uint64_t dA_hi = ptx::smem_desc(a_hi + aoff, Cfg::A_LBO, Cfg::A_SBO, Cfg::A_LAYOUT);
+                            const uint64_t dA_lo = ptx::smem_desc(a_lo + aoff, Cfg::A_LBO, Cfg::A_SBO, Cfg::A_LAYOUT);
                             const uint64_t dB_hi = ptx::smem_desc(b_hi + boff, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
                             const uint64_t dB_lo = ptx::smem_desc(b_lo + boff, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
                             const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
@@ -241,32 +255,53 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 uint8_t* oa_lo = o + Cfg::AOP_BYTES;
                 uint8_t* ob_hi = o + 2 * Cfg::AOP_BYTES;
                 uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
-                // A: warp sw handles k rows sw, sw+4, ...; lane handles m = 4*lane .. +3
+                if (ALAY == A_K_SW128) {
+                    // A K-major: one m row (32 k) per thread, 4 k per 16-byte chunk
+                    const uint32_t mrow = tid;
+#pragma unroll
+                    for (int j = 0; j < Cfg::BK / 4; ++j) {
+                        const float* col = reinterpret_cast<const float*>(fa) + (4 * j) * Cfg::BM + mrow;
+                        uint4 hv, lv;
+                        split_tf32(col[0], hv.x, lv.x);
+                        split_tf32(col[Cfg::BM], hv.y, lv.y);
+                        split_tf32(col[2 * Cfg::BM], hv.z, lv.z);
+                        split_tf32(col[3 * Cfg::BM], hv.w, lv.w);
+                        const uint32_t off = mrow * Cfg::B_ROW + ((j ^ (mrow & 7)) << 4);
+                        *reinterpret_cast<uint4*>(oa_hi + off) = hv;
+                        *reinterpret_cast<uint4*>(oa_lo + off) = lv;
+                    }
+                } else {
+                // A MN-major: warp sw handles k rows sw, sw+4, ...; lane handles m = 4*lane .. +3
 #pragma unroll
                 for (int kk = 0; kk < Cfg::BK / 4; ++kk) {
                     const uint32_t k = sw + 4 * kk;
                     const float4 v = *reinterpret_cast<const float4*>(fa + k * 512 + lane * 16);
-                    const uint32_t g = k >> 3, kr = k & 7;
                     if (MODE == 0) {
+                        const uint32_t g = k >> 3, kr = k & 7;
                         uint32_t h01, l01, h23, l23;
                         split_fp16x2(v.x, v.y, h01, l01);
                         split_fp16x2(v.z, v.w, h23, l23);
                         nonfinite |= f16x2_nonfinite(h01) | f16x2_nonfinite(h23);
                         const uint32_t mblk = lane >> 4, chunk = (lane & 15) >> 1;
-                        const uint32_t off = g * Cfg::A_SBO + mblk * 1024 + kr * 128 + ((chunk ^ kr) << 4) + (lane & 1) * 8;
+                        const uint32_t off = g * Cfg::A_SBO + mblk * Cfg::A_LBO + kr * 128 + ((chunk ^ kr) << 4) + (lane & 1) * 8;
                         *reinterpret_cast<uint2*>(oa_hi + off) = make_uint2(h01, h23);
                         *reinterpret_cast<uint2*>(oa_lo + off) = make_uint2(l01, l23);
                     } else {
+                        // SWIZZLE_128B_BASE32B: 32 m x 4 k atoms of 512 B, 32-byte units
+                        // (address bits [5,7)) XORed with the k row in the atom (bits [7,9))
+                        const uint32_t g = k >> 2, kr = k & 3;
                         uint4 h, l;
                         split_tf32(v.x, h.x, l.x);
                         split_tf32(v.y, h.y, l.y);
                         split_tf32(v.z, h.z, l.z);
                         split_tf32(v.w, h.w, l.w);
-                        const uint32_t mblk = lane >> 3, chunk = lane & 7;
-                        const uint32_t off = g * Cfg::A_SBO + mblk * 1024 + kr * 128 + ((chunk ^ kr) << 4);
+                        const uint32_t mblk = lane >> 3;
+                        const uint32_t inrow = (lane & 7) * 16;
+                        const uint32_t off = g * Cfg::A_SBO + mblk * Cfg::A_LBO + kr * 128 + (inrow ^ (kr << 5));
                         *reinterpret_cast<uint4*>(oa_hi + off) = h;
                         *reinterpret_cast<uint4*>(oa_lo + off) = l;
                     }
+                }
                 }
                 // B: one n row (32 k) per thread
 #pragma unroll

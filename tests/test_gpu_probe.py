@@ -65,7 +65,7 @@ def _probe(mode):
     for key, v in res.items():
         e = exact[key]
         out[key] = {"got": v.hex(), "exact": float(e).hex(),
-                    "err_ulps": (v - e) / np.spacing(np.float32(abs(e)))}
+                    "err_ulps": float((v - e) / np.spacing(np.float32(abs(e))))}
     rz = 1 + 2.0 ** -23
     rn = 1 + 2.0 ** -22
     out["S213_reading"] = ("RZ" if res["same_instr_1+3u"] == rz else
