@@ -41,7 +41,7 @@ EncodeTiledFn encode_fn()
 struct DeviceInfo {
     int ok = -1;  // -1 unknown, 0 not sm_100, 1 sm_100
     int sms = 0;
-    bool attr_set[8] = {};
+    bool attr_set[16] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -66,13 +66,14 @@ emu_status device_check(int& dev, int& sms)
     return d.ok == 1 ? EMU_STATUS_SUCCESS : EMU_STATUS_ARCH_MISMATCH;
 }
 
-template <int MODE, int BN, int ALAY>
+template <int MODE, int BN, int ALAY, bool RANGE>
 emu_status ensure_smem_attr(int dev)
 {
     std::lock_guard<std::mutex> lk(g_dev_mu);
-    const int slot = MODE * 4 + ALAY;
+    const int slot = (MODE * 4 + ALAY) * 2 + (RANGE ? 1 : 0);
     if (g_dev[dev].attr_set[slot]) return EMU_STATUS_SUCCESS;
-    if (cudaFuncSetAttribute(emu::emu_sgemm_kernel<MODE, BN, ALAY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)emu::GemmCfg<MODE, BN, ALAY>::SMEM_BYTES) != cudaSuccess)
         return EMU_STATUS_CUDA_ERROR;
     g_dev[dev].attr_set[slot] = true;
@@ -144,14 +145,14 @@ emu_status launch_status(cudaError_t e)
     return EMU_STATUS_LAUNCH_FAILED;
 }
 
-template <int MODE, int ALAY>
+template <int MODE, int ALAY, bool RANGE>
 emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
                     const float* B, int ldb, long long strideB, float beta, float* C, int ldc, long long strideC,
                     int batch, cudaStream_t stream, unsigned* range_flag, int kblock, unsigned flags)
 {
     constexpr int BN = 128;
     using Cfg = emu::GemmCfg<MODE, BN, ALAY>;
-    emu_status st = ensure_smem_attr<MODE, BN, ALAY>(dev);
+    emu_status st = ensure_smem_attr<MODE, BN, ALAY, RANGE>(dev);
     if (st != EMU_STATUS_SUCCESS) return st;
 
     const bool a_b = batch > 1 && strideA != 0;
@@ -181,7 +182,7 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     p.range_flag = MODE == 0 ? range_flag : nullptr;
 
     const long long grid = std::min<long long>(p.num_tiles, sms);
-    emu::emu_sgemm_kernel<MODE, BN, ALAY><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, p);
+    emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, p);
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
 }
@@ -247,17 +248,21 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     if ((unsigned long long)strideA * 4 >= (1ull << 40) || (unsigned long long)strideB * 4 >= (1ull << 40))
         return EMU_STATUS_NOT_SUPPORTED;
 
-    if (mode == EMU_SPLIT_FP16)
-        return run_gemm<0, emu::A_MN_SW128>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch,
-                           s, d_range_flag, kblock, flags);
+    if (mode == EMU_SPLIT_FP16) {
+        if (d_range_flag)
+            return run_gemm<0, emu::A_MN_SW128, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
+                                                      C, ldc, strideC, batch, s, d_range_flag, kblock, flags);
+        return run_gemm<0, emu::A_MN_SW128, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C,
+                                                   ldc, strideC, batch, s, nullptr, kblock, flags);
+    }
     static const bool tf32_mn = [] {
         const char* e = getenv("EMU_TF32_A_LAYOUT");   // tuning/diagnostics only
         return e && strcmp(e, "mn32") == 0;
     }();
     if (tf32_mn)
-        return run_gemm<1, emu::A_MN_SW128_32B>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C,
+        return run_gemm<1, emu::A_MN_SW128_32B, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C,
                                                 ldc, strideC, batch, s, nullptr, kblock, flags);
-    return run_gemm<1, emu::A_K_SW128>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc,
+    return run_gemm<1, emu::A_K_SW128, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc,
                                        strideC, batch, s, nullptr, kblock, flags);
 }
 

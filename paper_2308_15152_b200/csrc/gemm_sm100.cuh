@@ -1,38 +1,39 @@
 // gemm_sm100.cuh -- the emulated-SGEMM kernel for B200 (sm_100a).
 //
 // One persistent CTA per SM walks output tiles (batch, m-tile, n-tile) of
-// BM x BN = 128 x BN.  Warp roles (16 warps):
-//   warp 0      TMA producer: FP32 tiles of A (128 m x 32 k) and B (32 k x BN n)
-//               HBM -> shared memory ring `f32` (S32 stages), mbarrier complete_tx.
-//   warp 1      MMA issuer (one elected thread) + TMEM owner: per 16-k (FP16) or
-//               8-k (TF32) step three tcgen05.mma, P1 = A_hi B_hi -> D_hi,
-//               P2 = A_lo B_hi and P3 = A_hi B_lo -> D_corr (Eq. corr-5).
-//   warps 4-7   splitters: FP32 stage -> hi/lo operand tiles (Eqs. corr-1..4,
-//               P:479-488) written straight into the UMMA canonical layouts of
-//               the operand ring `op` (SOP stages).  This is the B200 form of the
-//               paper's split-on-load: the FP32 tile is read once
-//               from shared memory and each part is written once, in the layout
-//               the tensor core reads -- no separate FP16 staging copy and no
-//               re-layout pass.
-//   warps 8-15  combine/epilogue: every k-block of KB elements, tcgen05.ld of
-//               D_hi and D_corr, t = RN(D_hi + D_corr * 2^-11), C += t in FP32 RN
-//               on CUDA cores (the outside-of-TC accumulation of P:495, R#7/R#8);
-//               at the tile's end C = RN(alpha*C + RN(beta*C_old)), coalesced
-//               column-major stores.
+// BM x BN = 128 x BN.  Warp roles (18 warps, 576 threads):
+//   warp 0       TMA producer: FP32 tiles of A (128 m x 32 k) and B (32 k x BN n)
+//                HBM -> shared memory ring `f32` (S32 stages), mbarrier complete_tx.
+//   warp 1       MMA issuer (one elected thread) + TMEM owner: per 16-k (FP16) or
+//                8-k (TF32) step three tcgen05.mma, P1 = A_hi B_hi -> D_hi,
+//                P2 = A_lo B_hi and P3 = A_hi B_lo -> D_corr (Eq. corr-5).
+//   warps 2-9    splitters: FP32 stage -> hi/lo operand tiles (Eqs. corr-1..4,
+//                P:479-488) written straight into the UMMA canonical layouts of
+//                the operand ring `op` (SOP stages).  This is the B200 form of the
+//                paper's split-on-load: the FP32 tile is read once
+//                from shared memory and each part is written once, in the layout
+//                the tensor core reads -- no separate FP16 staging copy and no
+//                re-layout pass.  Two splitter warps per SM sub-partition.
+//   warps 10-17  combine/epilogue: every k-block of KB elements, tcgen05.ld of
+//                D_hi and D_corr, t = RN(D_hi + D_corr * 2^-11), C += t in FP32 RN
+//                on CUDA cores (the outside-of-TC accumulation of P:495, R#7/R#8);
+//                at the tile's end C = RN(alpha*C + RN(beta*C_old)), coalesced
+//                column-major stores.
 // TMEM: two accumulator buffers x (D_hi, D_corr) x BN columns = 512 columns, so
 // the MMA warp fills one buffer while the combine warps drain the other.
 //
 // Shared-memory layouts (all buffers 1024-byte aligned):
 //   f32 A  [32 k][128 m] fp32, plain (TMA box {128, 32}); 512-byte rows
 //   f32 B  [BN n][32 k]  fp32, TMA SWIZZLE_128B (box {32, BN}); 128-byte rows
-//   op A_hi/A_lo  MN-major SWIZZLE_128B canonical layout:
-//                 [k/8][m/(128B/esz)][k%8][128 B]; LBO = 1024 (next MN block),
-//                 SBO = (BM*esz/128)*1024 (next 8-k group)
+//   op A_hi/A_lo  FP16: MN-major SWIZZLE_128B [k/8][m/64][k%8][128 B], LBO 1024
+//                 (next 64-m block), SBO 2048 (next 8-k group).
+//                 TF32: K-major SWIZZLE_128B [m][32 k] (SBO 1024), or the 32-bit
+//                 MN-major SWIZZLE_128B_BASE32B [k/4][m/32][k%4][128 B] (variant).
 //   op B_hi/B_lo  K-major, one row of 32 k per n: FP16 64-byte rows SWIZZLE_64B
-//                 (SBO 512), TF32 128-byte rows SWIZZLE_128B (SBO 1024)
+//                 (SBO 512), TF32 128-byte rows SWIZZLE_128B (SBO 1024).
 // Swizzles are XORs on absolute shared addresses: 16-byte chunk bits [4,7)
-// (SW128) or [4,6) (SW64) ^= bits [7,10) / [7,9), which is what both TMA and
-// the UMMA descriptor apply.
+// (SW128) or [4,6) (SW64) ^= bits [7,10) / [7,9); BASE32B: 32-byte bits [5,7)
+// ^= bits [7,9) -- what both TMA and the UMMA descriptor apply.
 #pragma once
 
 #include <cstdint>
@@ -95,11 +96,13 @@ struct GemmCfg {
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
     static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + BAR_BYTES;
-    static constexpr int NUM_THREADS = 512;
-    static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 4;
-    static constexpr int EPI_WARP0 = 8, NUM_EPI_WARPS = 8;
+    static constexpr int SPLIT_WARP0 = 2, NUM_SPLIT_WARPS = 8;
+    static constexpr int EPI_WARP0 = 10, NUM_EPI_WARPS = 8;
+    static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
+    static constexpr int SPLIT_THREADS = 32 * NUM_SPLIT_WARPS;
     static_assert(2 * 2 * BN <= 512, "two (D_hi, D_corr) buffers must fit TMEM");
     static_assert(SMEM_BYTES <= 232448, "shared memory");
+    static_assert(BN == 128, "this kernel's splitter work division assumes BN = 128");
 };
 
 // tile index -> (batch, m-tile, n-tile); groups of up to 16 m-tiles walk the
@@ -118,14 +121,24 @@ __device__ __forceinline__ void tile_coords(const GemmParams& p, long long t, in
     nt = rr / gm;
 }
 
-template <int MODE, int BN, int ALAY>
-__global__ void __launch_bounds__(512, 1)
+// ------------------------------------------------------------ split helpers
+// Four FP32 values (consecutive along the 16-byte unit the layout stores) ->
+// FP16 hi/lo pairs: packed so element 0 is the low half.
+__device__ __forceinline__ void split4_fp16(const float4 v, uint2& h, uint2& l)
+{
+    split_fp16x2x2(v.x, v.y, v.z, v.w, h.x, h.y, l.x, l.y);
+}
+
+template <int MODE, int BN, int ALAY, bool RANGE>
+__global__ void __launch_bounds__(GemmCfg<MODE, BN, ALAY>::NUM_THREADS, 1)
 emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const GemmParams p)
 {
     using Cfg = GemmCfg<MODE, BN, ALAY>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // keep the pointer derived from the __shared__ array (so loads/stores stay
+    // LDS/STS) while aligning to 1024 bytes for the swizzled layouts
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* f32buf = smem;
     uint8_t* opbuf = smem + Cfg::S32 * Cfg::F32_STAGE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(opbuf + Cfg::SOP * Cfg::OP_STAGE);
@@ -143,10 +156,10 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < Cfg::S32; ++i) {
             ptx::mbar_init(&f32_full[i], 1);
-            ptx::mbar_init(&f32_empty[i], Cfg::NUM_SPLIT_WARPS * 32);
+            ptx::mbar_init(&f32_empty[i], Cfg::SPLIT_THREADS);
         }
         for (int i = 0; i < Cfg::SOP; ++i) {
-            ptx::mbar_init(&op_full[i], Cfg::NUM_SPLIT_WARPS * 32);
+            ptx::mbar_init(&op_full[i], Cfg::SPLIT_THREADS);
             ptx::mbar_init(&op_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -169,19 +182,18 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (ptx::elect_one()) {
-            const uint64_t pol_a = ptx::l2_policy_evict_last();
-            const uint64_t pol_b = ptx::l2_policy_evict_last();
+            const uint64_t pol = ptx::l2_policy_evict_last();
             uint32_t s = 0, ph = 0;
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
                 int b, mt, nt;
                 tile_coords(p, t, b, mt, nt);
                 const int ab = p.a_batched ? b : 0, bb = p.b_batched ? b : 0;
                 for (int ks = 0; ks < nks; ++ks) {
-                    ptx::mbar_wait(&f32_empty[s], ph ^ 1);
+                    ptx::mbar_wait_sleep(&f32_empty[s], ph ^ 1);
                     uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                     ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
-                    ptx::tma_load_3d(dst, &tmA, &f32_full[s], mt * Cfg::BM, ks * Cfg::BK, ab, pol_a);
-                    ptx::tma_load_3d(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK, nt * BN, bb, pol_b);
+                    ptx::tma_load_3d(dst, &tmA, &f32_full[s], mt * Cfg::BM, ks * Cfg::BK, ab, pol);
+                    ptx::tma_load_3d(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK, nt * BN, bb, pol);
                     if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                 }
             }
@@ -210,8 +222,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                         for (int st = 0; st < Cfg::NSTEPS; ++st) {
                             const uint32_t aoff = st * Cfg::A_STEP;
-                            // B: K-major, one K step = 32 bytes along the swizzled row
-                            const uint32_t boff = st * 32;
+                            const uint32_t boff = st * 32;   // K-major: 32 bytes along the swizzled row
                             const uint64_t dA_hi = ptx::smem_desc(a_hi + aoff, Cfg::A_LBO, Cfg::A_SBO, Cfg::A_LAYOUT);
                             const uint64_t dA_lo = ptx::smem_desc(a_lo + aoff, Cfg::A_LBO, Cfg::A_SBO, Cfg::A_LAYOUT);
                             const uint64_t dB_hi = ptx::smem_desc(b_hi + boff, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
@@ -239,9 +250,10 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
     } else if (warp >= Cfg::SPLIT_WARP0 && warp < Cfg::SPLIT_WARP0 + Cfg::NUM_SPLIT_WARPS) {
-        // ------------------------------------------------ splitters
-        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;   // 0..127
-        const uint32_t sw = tid >> 5;
+        // ------------------------------------------------ splitters (256 threads)
+        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;   // 0..255
+        const uint32_t sw = tid >> 5;                                 // 0..7
+        const uint32_t row = tid & 127, half = tid >> 7;              // K-major rows: half of the 32 k each
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
         uint32_t nonfinite = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -256,78 +268,78 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 uint8_t* ob_hi = o + 2 * Cfg::AOP_BYTES;
                 uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
                 if (ALAY == A_K_SW128) {
-                    // A K-major: one m row (32 k) per thread, 4 k per 16-byte chunk
-                    const uint32_t mrow = tid;
+                    // A K-major (TF32): thread = (m row, 16-k half); 4 k per 16-byte chunk
 #pragma unroll
-                    for (int j = 0; j < Cfg::BK / 4; ++j) {
-                        const float* col = reinterpret_cast<const float*>(fa) + (4 * j) * Cfg::BM + mrow;
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const uint32_t j = half * 4 + jj;
+                        const float* col = reinterpret_cast<const float*>(fa) + (4 * j) * Cfg::BM + row;
                         uint4 hv, lv;
                         split_tf32(col[0], hv.x, lv.x);
                         split_tf32(col[Cfg::BM], hv.y, lv.y);
                         split_tf32(col[2 * Cfg::BM], hv.z, lv.z);
                         split_tf32(col[3 * Cfg::BM], hv.w, lv.w);
-                        const uint32_t off = mrow * Cfg::B_ROW + ((j ^ (mrow & 7)) << 4);
+                        const uint32_t off = row * Cfg::B_ROW + ((j ^ (row & 7)) << 4);
                         *reinterpret_cast<uint4*>(oa_hi + off) = hv;
                         *reinterpret_cast<uint4*>(oa_lo + off) = lv;
                     }
                 } else {
-                // A MN-major: warp sw handles k rows sw, sw+4, ...; lane handles m = 4*lane .. +3
+                    // A MN-major: warp sw handles k rows sw, sw+8, ...; lane handles m = 4*lane .. +3
 #pragma unroll
-                for (int kk = 0; kk < Cfg::BK / 4; ++kk) {
-                    const uint32_t k = sw + 4 * kk;
-                    const float4 v = *reinterpret_cast<const float4*>(fa + k * 512 + lane * 16);
-                    if (MODE == 0) {
-                        const uint32_t g = k >> 3, kr = k & 7;
-                        uint32_t h01, l01, h23, l23;
-                        split_fp16x2(v.x, v.y, h01, l01);
-                        split_fp16x2(v.z, v.w, h23, l23);
-                        nonfinite |= f16x2_nonfinite(h01) | f16x2_nonfinite(h23);
-                        const uint32_t mblk = lane >> 4, chunk = (lane & 15) >> 1;
-                        const uint32_t off = g * Cfg::A_SBO + mblk * Cfg::A_LBO + kr * 128 + ((chunk ^ kr) << 4) + (lane & 1) * 8;
-                        *reinterpret_cast<uint2*>(oa_hi + off) = make_uint2(h01, h23);
-                        *reinterpret_cast<uint2*>(oa_lo + off) = make_uint2(l01, l23);
-                    } else {
-                        // SWIZZLE_128B_BASE32B: 32 m x 4 k atoms of 512 B, 32-byte units
-                        // (address bits [5,7)) XORed with the k row in the atom (bits [7,9))
-                        const uint32_t g = k >> 2, kr = k & 3;
-                        uint4 h, l;
-                        split_tf32(v.x, h.x, l.x);
-                        split_tf32(v.y, h.y, l.y);
-                        split_tf32(v.z, h.z, l.z);
-                        split_tf32(v.w, h.w, l.w);
-                        const uint32_t mblk = lane >> 3;
-                        const uint32_t inrow = (lane & 7) * 16;
-                        const uint32_t off = g * Cfg::A_SBO + mblk * Cfg::A_LBO + kr * 128 + (inrow ^ (kr << 5));
-                        *reinterpret_cast<uint4*>(oa_hi + off) = h;
-                        *reinterpret_cast<uint4*>(oa_lo + off) = l;
+                    for (int kk = 0; kk < Cfg::BK / 8; ++kk) {
+                        const uint32_t k = sw + 8 * kk;
+                        const float4 v = *reinterpret_cast<const float4*>(fa + k * 512 + lane * 16);
+                        if (MODE == 0) {
+                            const uint32_t g = k >> 3, kr = k & 7;
+                            uint2 h, l;
+                            split4_fp16(v, h, l);
+                            if (RANGE) nonfinite |= f16x2_nonfinite(h.x) | f16x2_nonfinite(h.y);
+                            const uint32_t mblk = lane >> 4, chunk = (lane & 15) >> 1;
+                            const uint32_t off = g * Cfg::A_SBO + mblk * Cfg::A_LBO + kr * 128 +
+                                                 ((chunk ^ kr) << 4) + (lane & 1) * 8;
+                            *reinterpret_cast<uint2*>(oa_hi + off) = h;
+                            *reinterpret_cast<uint2*>(oa_lo + off) = l;
+                        } else {
+                            // SWIZZLE_128B_BASE32B: 32 m x 4 k atoms of 512 B, 32-byte units
+                            // (address bits [5,7)) XORed with the k row in the atom (bits [7,9))
+                            const uint32_t g = k >> 2, kr = k & 3;
+                            uint4 h, l;
+                            split_tf32(v.x, h.x, l.x);
+                            split_tf32(v.y, h.y, l.y);
+                            split_tf32(v.z, h.z, l.z);
+                            split_tf32(v.w, h.w, l.w);
+                            const uint32_t mblk = lane >> 3;
+                            const uint32_t inrow = (lane & 7) * 16;
+                            const uint32_t off = g * Cfg::A_SBO + mblk * Cfg::A_LBO + kr * 128 + (inrow ^ (kr << 5));
+                            *reinterpret_cast<uint4*>(oa_hi + off) = h;
+                            *reinterpret_cast<uint4*>(oa_lo + off) = l;
+                        }
                     }
                 }
-                }
-                // B: one n row (32 k) per thread
-#pragma unroll
-                for (int rr = 0; rr < BN / 128; ++rr) {
-                    const uint32_t n = tid + rr * 128;
-                    const uint8_t* row = fb + n * 128;
+                // B: thread = (n row, 16-k half)
+                {
+                    const uint32_t n = row;
+                    const uint8_t* brow = fb + n * 128;
                     if (MODE == 0) {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {   // 8 k per 16-byte FP16 chunk
-                            const float4 v0 = *reinterpret_cast<const float4*>(row + (((2 * j) ^ (n & 7)) << 4));
-                            const float4 v1 = *reinterpret_cast<const float4*>(row + (((2 * j + 1) ^ (n & 7)) << 4));
-                            uint4 h, l;
-                            split_fp16x2(v0.x, v0.y, h.x, l.x);
-                            split_fp16x2(v0.z, v0.w, h.y, l.y);
-                            split_fp16x2(v1.x, v1.y, h.z, l.z);
-                            split_fp16x2(v1.z, v1.w, h.w, l.w);
-                            nonfinite |= f16x2_nonfinite(h.x) | f16x2_nonfinite(h.y) |
-                                         f16x2_nonfinite(h.z) | f16x2_nonfinite(h.w);
+                        for (int jj = 0; jj < 2; ++jj) {   // 8 k per 16-byte FP16 chunk
+                            const uint32_t j = half * 2 + jj;
+                            const float4 v0 = *reinterpret_cast<const float4*>(brow + (((2 * j) ^ (n & 7)) << 4));
+                            const float4 v1 = *reinterpret_cast<const float4*>(brow + (((2 * j + 1) ^ (n & 7)) << 4));
+                            uint2 h0, l0, h1, l1;
+                            split4_fp16(v0, h0, l0);
+                            split4_fp16(v1, h1, l1);
+                            if (RANGE)
+                                nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) |
+                                             f16x2_nonfinite(h1.x) | f16x2_nonfinite(h1.y);
                             const uint32_t off = n * 64 + ((j ^ ((n >> 1) & 3)) << 4);
-                            *reinterpret_cast<uint4*>(ob_hi + off) = h;
-                            *reinterpret_cast<uint4*>(ob_lo + off) = l;
+                            *reinterpret_cast<uint4*>(ob_hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+                            *reinterpret_cast<uint4*>(ob_lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {   // 4 k per 16-byte TF32 chunk
-                            const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (n & 7)) << 4));
+                        for (int jj = 0; jj < 4; ++jj) {   // 4 k per 16-byte TF32 chunk
+                            const uint32_t j = half * 4 + jj;
+                            const float4 v = *reinterpret_cast<const float4*>(brow + ((j ^ (n & 7)) << 4));
                             uint4 h, l;
                             split_tf32(v.x, h.x, l.x);
                             split_tf32(v.y, h.y, l.y);
@@ -346,7 +358,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 if (++sop == Cfg::SOP) { sop = 0; phop ^= 1; }
             }
         }
-        if (MODE == 0 && p.range_flag != nullptr) {
+        if (RANGE) {
             nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
             if (nonfinite && lane == 0) atomicOr(p.range_flag, 1u);
         }
@@ -366,36 +378,40 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
             for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                 const uint32_t buf = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-                ptx::mbar_wait(&acc_full[buf], aph);
+                ptx::mbar_wait_sleep(&acc_full[buf], aph);
                 ptx::tc_fence_after();
                 const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * BN + h * HALF;
 #pragma unroll
-                for (int c = 0; c < HALF / 16; ++c) {
-                    float vh[16], vc[16];
-                    ptx::tmem_ld16(taddr + c * 16, vh);
-                    ptx::tmem_ld16(taddr + BN + c * 16, vc);
+                for (int c = 0; c < HALF / 8; ++c) {
+                    float vh[8], vc[8];
+                    ptx::tmem_ld8(taddr + c * 8, vh);
+                    ptx::tmem_ld8(taddr + BN + c * 8, vc);
                     ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (int j = 0; j < 8; ++j) {
                         const float tt = p.corr ? fmaf(vc[j], scale, vh[j]) : vh[j];
-                        creg[c * 16 + j] = __fadd_rn(creg[c * 16 + j], tt);
+                        creg[c * 8 + j] = __fadd_rn(creg[c * 8 + j], tt);
                     }
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&acc_empty[buf]);
             }
             // epilogue: C = RN(alpha*C + RN(beta*C_old)), column-major, coalesced per column
-            const int row = mt * Cfg::BM + (int)(q * 32 + lane);
+            const int r = mt * Cfg::BM + (int)(q * 32 + lane);
             const int col0 = nt * BN + (int)(h * HALF);
-            if (row < p.m) {
-                float* cp = p.C + (long long)b * p.strideC + row + (long long)col0 * p.ldc;
+            if (r < p.m) {
+                float* cp = p.C + (long long)b * p.strideC + r + (long long)col0 * p.ldc;
+                if (p.beta != 0.0f) {
 #pragma unroll
-                for (int j = 0; j < HALF; ++j) {
-                    if (col0 + j < p.n) {
-                        float* dst = cp + (long long)j * p.ldc;
-                        const float bc = p.beta != 0.0f ? __fmul_rn(p.beta, *dst) : 0.0f;
-                        *dst = fmaf(p.alpha, creg[j], bc);
-                    }
+                    for (int j = 0; j < HALF; ++j)
+                        if (col0 + j < p.n) {
+                            float* dst = cp + (long long)j * p.ldc;
+                            *dst = fmaf(p.alpha, creg[j], __fmul_rn(p.beta, *dst));
+                        }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < HALF; ++j)
+                        if (col0 + j < p.n) cp[(long long)j * p.ldc] = fmaf(p.alpha, creg[j], 0.0f);
                 }
             }
         }

@@ -32,15 +32,37 @@ __device__ __forceinline__ void f16x2_to_f32x2(uint32_t h, float& x0, float& x1)
         : "=f"(x0), "=f"(x1) : "r"(h));
 }
 
+// (x0 - h0, x1 - h1) * 2^11 on the packed FP32x2 pipe (FADD2, FMUL2): each lane
+// is one IEEE binary32 operation with round-to-nearest, never contracted
+__device__ __forceinline__ void sub_mul2048_f32x2(float x0, float x1, float h0, float h1, float& r0, float& r1)
+{
+    asm("{\n\t.reg .b64 a, b, d;\n\t"
+        "mov.b64 a, {%2, %3};\n\t"
+        "mov.b64 b, {%4, %5};\n\t"
+        "sub.rn.f32x2 d, a, b;\n\t"
+        "mov.b64 b, {%6, %6};\n\t"
+        "mul.rn.f32x2 d, d, b;\n\t"
+        "mov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r0), "=f"(r1) : "f"(x0), "f"(x1), "f"(h0), "f"(h1), "f"(2048.0f));
+}
+
 // Eqs. corr-1/corr-2 for two elements: packed hi and packed lo (low half = x0)
 __device__ __forceinline__ void split_fp16x2(float x0, float x1, uint32_t& hi, uint32_t& lo)
 {
     hi = f32x2_to_f16x2_rn(x0, x1);
     float h0, h1;
     f16x2_to_f32x2(hi, h0, h1);
-    const float r0 = __fmul_rn(__fsub_rn(x0, h0), 2048.0f);
-    const float r1 = __fmul_rn(__fsub_rn(x1, h1), 2048.0f);
+    float r0, r1;
+    sub_mul2048_f32x2(x0, x1, h0, h1, r0, r1);
     lo = f32x2_to_f16x2_rn(r0, r1);
+}
+
+// four elements: (x0, x1) -> h01/l01, (x2, x3) -> h23/l23
+__device__ __forceinline__ void split_fp16x2x2(float x0, float x1, float x2, float x3, uint32_t& h01,
+                                               uint32_t& h23, uint32_t& l01, uint32_t& l23)
+{
+    split_fp16x2(x0, x1, h01, l01);
+    split_fp16x2(x2, x3, h23, l23);
 }
 
 // 1 if either binary16 half of `h` is +-Inf or NaN (exponent field all ones)
