@@ -72,8 +72,11 @@ typedef enum {
  *   overlap A or B.
  *   Quick returns: m == 0 || n == 0 || batch == 0 -> SUCCESS, nothing
  *   launched; k == 0 || alpha == 0 -> C = RN(beta*C) (beta == 0 writes +0).
- *   Domain (else NOT_SUPPORTED): A, B 16-byte aligned; lda, ldb, strideA,
- *   strideB multiples of 4 elements (tensor-map strides are 16-byte units).
+ *   Any alignment and leading dimension is accepted.  When A and B are
+ *   16-byte aligned and lda, ldb, strideA, strideB are multiples of 4
+ *   elements, FP32 tiles are staged by TMA (tensor-map strides are 16-byte
+ *   units); otherwise the splitter warps load them directly (slower path,
+ *   identical results).
  *   FP16 mode: |A|, |B| < 65520 and finite, else those outputs are
  *   non-finite (R#4); pass d_range_flag to emu_sgemm_batched_ex to detect it.
  */

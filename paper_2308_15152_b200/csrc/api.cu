@@ -41,7 +41,7 @@ EncodeTiledFn encode_fn()
 struct DeviceInfo {
     int ok = -1;  // -1 unknown, 0 not sm_100, 1 sm_100
     int sms = 0;
-    bool attr_set[16] = {};
+    bool attr_set[32] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -66,13 +66,13 @@ emu_status device_check(int& dev, int& sms)
     return d.ok == 1 ? EMU_STATUS_SUCCESS : EMU_STATUS_ARCH_MISMATCH;
 }
 
-template <int MODE, int BN, int ALAY, bool RANGE>
+template <int MODE, int BN, int ALAY, bool RANGE, bool LDG>
 emu_status ensure_smem_attr(int dev)
 {
     std::lock_guard<std::mutex> lk(g_dev_mu);
-    const int slot = (MODE * 4 + ALAY) * 2 + (RANGE ? 1 : 0);
+    const int slot = ((MODE * 4 + ALAY) * 2 + (RANGE ? 1 : 0)) * 2 + (LDG ? 1 : 0);
     if (g_dev[dev].attr_set[slot]) return EMU_STATUS_SUCCESS;
-    if (cudaFuncSetAttribute(emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE>,
+    if (cudaFuncSetAttribute(emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE, LDG>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)emu::GemmCfg<MODE, BN, ALAY>::SMEM_BYTES) != cudaSuccess)
         return EMU_STATUS_CUDA_ERROR;
@@ -145,27 +145,29 @@ emu_status launch_status(cudaError_t e)
     return EMU_STATUS_LAUNCH_FAILED;
 }
 
-template <int MODE, int ALAY, bool RANGE>
+template <int MODE, int ALAY, bool RANGE, bool LDG>
 emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
                     const float* B, int ldb, long long strideB, float beta, float* C, int ldc, long long strideC,
                     int batch, cudaStream_t stream, unsigned* range_flag, int kblock, unsigned flags)
 {
     constexpr int BN = 128;
     using Cfg = emu::GemmCfg<MODE, BN, ALAY>;
-    emu_status st = ensure_smem_attr<MODE, BN, ALAY, RANGE>(dev);
+    emu_status st = ensure_smem_attr<MODE, BN, ALAY, RANGE, LDG>(dev);
     if (st != EMU_STATUS_SUCCESS) return st;
 
     const bool a_b = batch > 1 && strideA != 0;
     const bool b_b = batch > 1 && strideB != 0;
     CUtensorMap tmA, tmB;
+    std::memset(&tmA, 0, sizeof(tmA));
+    std::memset(&tmB, 0, sizeof(tmB));
     // dim-2 stride: any valid value when the batch extent is 1
     const uint64_t sA = a_b ? (uint64_t)strideA : (((uint64_t)lda * (uint64_t)k + 3) & ~uint64_t(3));
     const uint64_t sB = b_b ? (uint64_t)strideB : (((uint64_t)ldb * (uint64_t)n + 3) & ~uint64_t(3));
-    if (!make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA, Cfg::BM, Cfg::BK,
-                  CU_TENSOR_MAP_SWIZZLE_NONE))
+    if (!LDG && !make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA, Cfg::BM,
+                          Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE))
         return EMU_STATUS_NOT_SUPPORTED;
-    if (!make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB, Cfg::BK, BN,
-                  CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!LDG && !make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB, Cfg::BK,
+                          BN, CU_TENSOR_MAP_SWIZZLE_128B))
         return EMU_STATUS_NOT_SUPPORTED;
 
     emu::GemmParams p;
@@ -180,9 +182,11 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     p.kb_stages = (kblock > 0 ? kblock : 64) / Cfg::BK;
     p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
     p.range_flag = MODE == 0 ? range_flag : nullptr;
+    p.A = A; p.B = B; p.lda = lda; p.ldb = ldb;
+    p.strideA = a_b ? strideA : 0; p.strideB = b_b ? strideB : 0;
 
     const long long grid = std::min<long long>(p.num_tiles, sms);
-    emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, p);
+    emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE, LDG><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, p);
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
 }
@@ -241,29 +245,35 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
         g_last_launches = 1;
         return launch_status(cudaGetLastError());
     }
-    // ---- domain of the TMA path ----
-    if (!aligned16(A) || !aligned16(B)) return EMU_STATUS_NOT_SUPPORTED;
-    if (lda % 4 != 0 || ldb % 4 != 0) return EMU_STATUS_NOT_SUPPORTED;
-    if ((batch > 1 && strideA % 4 != 0) || (batch > 1 && strideB % 4 != 0)) return EMU_STATUS_NOT_SUPPORTED;
-    if ((unsigned long long)strideA * 4 >= (1ull << 40) || (unsigned long long)strideB * 4 >= (1ull << 40))
-        return EMU_STATUS_NOT_SUPPORTED;
-
+    // ---- TMA path when its alignment domain holds, else the direct-load path ----
+    const bool tma_ok = aligned16(A) && aligned16(B) && lda % 4 == 0 && ldb % 4 == 0 &&
+                        (batch <= 1 || strideA == 0 || strideA % 4 == 0) &&
+                        (batch <= 1 || strideB == 0 || strideB % 4 == 0) &&
+                        (unsigned long long)strideA * 4 < (1ull << 40) && (unsigned long long)strideB * 4 < (1ull << 40);
+    static const int force_ldg = [] {
+        const char* e = getenv("EMU_FORCE_LDG");   // testing/diagnostics only
+        return e && strcmp(e, "1") == 0;
+    }();
+    const bool ldg = !tma_ok || force_ldg;
+#define EMU_RUN(MODE_, ALAY_, RANGE_, LDG_)                                                                         \
+    return run_gemm<MODE_, ALAY_, RANGE_, LDG_>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, \
+                                                ldc, strideC, batch, s, d_range_flag, kblock, flags)
     if (mode == EMU_SPLIT_FP16) {
-        if (d_range_flag)
-            return run_gemm<0, emu::A_MN_SW128, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
-                                                      C, ldc, strideC, batch, s, d_range_flag, kblock, flags);
-        return run_gemm<0, emu::A_MN_SW128, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C,
-                                                   ldc, strideC, batch, s, nullptr, kblock, flags);
+        if (d_range_flag) {
+            if (ldg) EMU_RUN(0, emu::A_MN_SW128, true, true);
+            EMU_RUN(0, emu::A_MN_SW128, true, false);
+        }
+        if (ldg) EMU_RUN(0, emu::A_MN_SW128, false, true);
+        EMU_RUN(0, emu::A_MN_SW128, false, false);
     }
     static const bool tf32_mn = [] {
         const char* e = getenv("EMU_TF32_A_LAYOUT");   // tuning/diagnostics only
         return e && strcmp(e, "mn32") == 0;
     }();
-    if (tf32_mn)
-        return run_gemm<1, emu::A_MN_SW128_32B, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C,
-                                                ldc, strideC, batch, s, nullptr, kblock, flags);
-    return run_gemm<1, emu::A_K_SW128, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc,
-                                       strideC, batch, s, nullptr, kblock, flags);
+    if (ldg) EMU_RUN(1, emu::A_K_SW128, false, true);
+    if (tf32_mn) EMU_RUN(1, emu::A_MN_SW128_32B, false, false);
+    EMU_RUN(1, emu::A_K_SW128, false, false);
+#undef EMU_RUN
 }
 
 __attribute__((visibility("default"))) emu_status emu_sgemm_batched(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,

@@ -56,6 +56,10 @@ struct GemmParams {
     int kb_stages;                // KB / 32
     int corr;                     // 1 = the paper's method; 0 = "correction off" control
     unsigned int* range_flag;     // nullable (FP16 mode only)
+    // direct-load (LDG) variant only: operands read by the splitter warps
+    const float* A;
+    const float* B;
+    long long lda, ldb, strideA, strideB;   // elements; stride 0 = shared operand
 };
 
 // A operand layouts in the operand ring
@@ -129,7 +133,11 @@ __device__ __forceinline__ void split4_fp16(const float4 v, uint2& h, uint2& l)
     split_fp16x2x2(v.x, v.y, v.z, v.w, h.x, h.y, l.x, l.y);
 }
 
-template <int MODE, int BN, int ALAY, bool RANGE>
+// LDG = false: TMA stages FP32 tiles in shared memory (the fast path; needs
+// 16-byte aligned bases and leading dimensions / strides in 16-byte units).
+// LDG = true: the splitter warps read FP32 operands straight from global memory
+// with bounds checks (any alignment, any lda/ldb); the TMA warp idles.
+template <int MODE, int BN, int ALAY, bool RANGE, bool LDG>
 __global__ void __launch_bounds__(GemmCfg<MODE, BN, ALAY>::NUM_THREADS, 1)
 emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const GemmParams p)
@@ -181,7 +189,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
-        if (ptx::elect_one()) {
+        if (!LDG && ptx::elect_one()) {
             const uint64_t pol = ptx::l2_policy_evict_last();
             uint32_t s = 0, ph = 0;
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -257,11 +265,39 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
         uint32_t nonfinite = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            int tb = 0, tmt = 0, tnt = 0;
+            if (LDG) tile_coords(p, t, tb, tmt, tnt);
+            const float* gA = LDG ? p.A + (long long)tb * p.strideA : nullptr;
+            const float* gB = LDG ? p.B + (long long)tb * p.strideB : nullptr;
             for (int ks = 0; ks < nks; ++ks) {
-                ptx::mbar_wait(&f32_full[s32], ph32);
+                if (!LDG) ptx::mbar_wait(&f32_full[s32], ph32);
                 ptx::mbar_wait(&op_empty[sop], phop ^ 1);
                 const uint8_t* fa = f32buf + s32 * Cfg::F32_STAGE;
                 const uint8_t* fb = fa + Cfg::A32_BYTES;
+                const int m0 = tmt * Cfg::BM, n0 = tnt * BN, k0 = ks * Cfg::BK;
+                // FP32 A(m0 + m, k0 + k) and B(k0 + k, n0 + n): shared-memory stage or global
+                auto a1 = [&](uint32_t m, uint32_t k) -> float {
+                    if (LDG) {
+                        const int gm = m0 + (int)m, gk = k0 + (int)k;
+                        return (gm < p.m && gk < p.k) ? __ldg(gA + gm + (long long)gk * p.lda) : 0.0f;
+                    }
+                    return reinterpret_cast<const float*>(fa)[k * Cfg::BM + m];
+                };
+                auto a4 = [&](uint32_t m, uint32_t k) -> float4 {   // A(m..m+3, k)
+                    if (LDG) return make_float4(a1(m, k), a1(m + 1, k), a1(m + 2, k), a1(m + 3, k));
+                    return *reinterpret_cast<const float4*>(fa + k * 512 + m * 4);
+                };
+                auto b4 = [&](uint32_t n, uint32_t c) -> float4 {   // B(4c..4c+3, n)
+                    if (LDG) {
+                        const int gn = n0 + (int)n, gk = k0 + 4 * (int)c;
+                        const float* col = gB + (long long)gn * p.ldb + gk;
+                        const bool okn = gn < p.n;
+                        return make_float4(okn && gk < p.k ? __ldg(col) : 0.0f, okn && gk + 1 < p.k ? __ldg(col + 1) : 0.0f,
+                                           okn && gk + 2 < p.k ? __ldg(col + 2) : 0.0f,
+                                           okn && gk + 3 < p.k ? __ldg(col + 3) : 0.0f);
+                    }
+                    return *reinterpret_cast<const float4*>(fb + n * 128 + ((c ^ (n & 7)) << 4));
+                };
                 uint8_t* o = opbuf + sop * Cfg::OP_STAGE;
                 uint8_t* oa_hi = o;
                 uint8_t* oa_lo = o + Cfg::AOP_BYTES;
@@ -272,12 +308,11 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int jj = 0; jj < 4; ++jj) {
                         const uint32_t j = half * 4 + jj;
-                        const float* col = reinterpret_cast<const float*>(fa) + (4 * j) * Cfg::BM + row;
                         uint4 hv, lv;
-                        split_tf32(col[0], hv.x, lv.x);
-                        split_tf32(col[Cfg::BM], hv.y, lv.y);
-                        split_tf32(col[2 * Cfg::BM], hv.z, lv.z);
-                        split_tf32(col[3 * Cfg::BM], hv.w, lv.w);
+                        split_tf32(a1(row, 4 * j), hv.x, lv.x);
+                        split_tf32(a1(row, 4 * j + 1), hv.y, lv.y);
+                        split_tf32(a1(row, 4 * j + 2), hv.z, lv.z);
+                        split_tf32(a1(row, 4 * j + 3), hv.w, lv.w);
                         const uint32_t off = row * Cfg::B_ROW + ((j ^ (row & 7)) << 4);
                         *reinterpret_cast<uint4*>(oa_hi + off) = hv;
                         *reinterpret_cast<uint4*>(oa_lo + off) = lv;
@@ -287,7 +322,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int kk = 0; kk < Cfg::BK / 8; ++kk) {
                         const uint32_t k = sw + 8 * kk;
-                        const float4 v = *reinterpret_cast<const float4*>(fa + k * 512 + lane * 16);
+                        const float4 v = a4(lane * 4, k);
                         if (MODE == 0) {
                             const uint32_t g = k >> 3, kr = k & 7;
                             uint2 h, l;
@@ -318,13 +353,12 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 // B: thread = (n row, 16-k half)
                 {
                     const uint32_t n = row;
-                    const uint8_t* brow = fb + n * 128;
                     if (MODE == 0) {
 #pragma unroll
                         for (int jj = 0; jj < 2; ++jj) {   // 8 k per 16-byte FP16 chunk
                             const uint32_t j = half * 2 + jj;
-                            const float4 v0 = *reinterpret_cast<const float4*>(brow + (((2 * j) ^ (n & 7)) << 4));
-                            const float4 v1 = *reinterpret_cast<const float4*>(brow + (((2 * j + 1) ^ (n & 7)) << 4));
+                            const float4 v0 = b4(n, 2 * j);
+                            const float4 v1 = b4(n, 2 * j + 1);
                             uint2 h0, l0, h1, l1;
                             split4_fp16(v0, h0, l0);
                             split4_fp16(v1, h1, l1);
@@ -339,7 +373,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                         for (int jj = 0; jj < 4; ++jj) {   // 4 k per 16-byte TF32 chunk
                             const uint32_t j = half * 4 + jj;
-                            const float4 v = *reinterpret_cast<const float4*>(brow + ((j ^ (n & 7)) << 4));
+                            const float4 v = b4(n, j);
                             uint4 h, l;
                             split_tf32(v.x, h.x, l.x);
                             split_tf32(v.y, h.y, l.y);
@@ -353,7 +387,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 ptx::fence_proxy_async_smem();        // our st.shared -> visible to UMMA
                 ptx::mbar_arrive(&op_full[sop]);
-                ptx::mbar_arrive(&f32_empty[s32]);
+                if (!LDG) ptx::mbar_arrive(&f32_empty[s32]);
                 if (++s32 == Cfg::S32) { s32 = 0; ph32 ^= 1; }
                 if (++sop == Cfg::SOP) { sop = 0; phop ^= 1; }
             }

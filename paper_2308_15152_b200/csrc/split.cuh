@@ -9,6 +9,8 @@
 //   _rn intrinsics so they can never be contracted into an FMA.
 // TF32: hi = RNE_tf32(x), lo = RNE_tf32(x - hi), with the low 13 bits cleared
 //   explicitly so the tensor core's treatment of them is irrelevant (R#6).
+//   The hardware cvt.rn.tf32.f32 is used; tf32_rn_bits is the integer form it
+//   was checked against.
 #pragma once
 
 #include <cstdint>
@@ -81,10 +83,19 @@ __device__ __forceinline__ uint32_t tf32_rn_bits(uint32_t u)
     return special ? s : r;
 }
 
+// cvt.rn.tf32.f32 (one F2FP.TF32.F32.PACK_B) -- verified on a B200 to equal
+// tf32_rn_bits on all 2^32 inputs (tools/probe_tf32_cvt.cu, NaN by NaN-ness)
+__device__ __forceinline__ uint32_t tf32_rn_cvt(float x)
+{
+    uint32_t r;
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo)
 {
-    hi = tf32_rn_bits(__float_as_uint(x));
-    lo = tf32_rn_bits(__float_as_uint(__fsub_rn(x, __uint_as_float(hi))));
+    hi = tf32_rn_cvt(x);
+    lo = tf32_rn_cvt(__fsub_rn(x, __uint_as_float(hi)));
 }
 
 }  // namespace emu

@@ -251,14 +251,24 @@ def test_host_entry_matches_device_entry(mode):
     assert np.array_equal(Ch, Cd)
 
 
-def test_not_supported_domain():
+@pytest.mark.parametrize("mode", MODES)
+def test_unaligned_operands_direct_load_path(mode):
+    """lda/ldb not multiples of 4 and misaligned bases take the direct-load
+    (non-TMA) path: same parity bars."""
     import torch
     import paper_2308_15152_b200 as emu
-    A = torch.zeros(64 * 65, device="cuda")
-    C = torch.zeros(64 * 64, device="cuda")
-    with pytest.raises(emu.EmuError) as e:      # lda not a multiple of 4
-        emu.emu_sgemm_batched(63, 64, 64, 1.0, A, 63, 0, A, 64, 0, 0.0, C, 63, 0, 1, "fp16")
-    assert e.value.status == 2
-    with pytest.raises(emu.EmuError) as e:      # misaligned base
-        emu.emu_sgemm_batched(64, 64, 64, 1.0, A.data_ptr() + 4, 64, 0, A, 64, 0, 0.0, C, 64, 0, 1, "fp16")
-    assert e.value.status == 2
+    m, n, k = 63, 61, 77
+    A, B = workloads.make_operands(1, m, n, k, seed=31, lda=65, ldb=78)
+    _cmp(mode, A, B, m, n, k)
+    # misaligned base pointers (offset by one float) with aligned ld
+    A2, B2 = workloads.make_operands(1, m, n, k, seed=32, lda=64, ldb=80)
+    dA = torch.zeros(A2.size + 1, device="cuda")
+    dB = torch.zeros(B2.size + 1, device="cuda")
+    dA[1:] = torch.from_numpy(A2.ravel()).cuda()
+    dB[1:] = torch.from_numpy(B2.ravel()).cuda()
+    dC = torch.empty((n, m), device="cuda")
+    emu.emu_sgemm(m, n, k, 1.0, dA.data_ptr() + 4, 64, dB.data_ptr() + 4, 80, 0.0, dC, m, mode)
+    torch.cuda.synchronize()
+    ref = oracle.emu_gemm(mode, A2, B2, m, n, k)[0]
+    tol = tolerance(mode, A2, B2, m, n, k)[0]
+    assert np.all(np.abs(dC.cpu().numpy().astype(np.float64) - ref) <= tol)
