@@ -110,10 +110,12 @@ emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha,
 /*
  * emu_sgemm_batched_host -- the same operation on HOST buffers (pinned or
  * pageable, column-major as above, C read only if beta != 0): stages the
- * operands into device memory it allocates on `stream`, runs the device path,
- * copies C back and synchronises `stream` before returning.  Copies and
- * compute run in stream order.  Same domain and errors;
- * allocation failure -> EMU_STATUS_CUDA_ERROR.
+ * operands into a per-device device workspace the library keeps (grow-only),
+ * runs the device path, copies C back and synchronises `stream` before
+ * returning.  Batches of >= 16 problems are processed in 8 chunks on two
+ * internal streams so the copies of one chunk overlap the kernel of the next
+ * (work is ordered after prior work on `stream`).  Calls are serialised per
+ * device.  Same errors; allocation failure -> EMU_STATUS_CUDA_ERROR.
  */
 emu_status emu_sgemm_batched_host(int m, int n, int k, float alpha,
                                   const float* A, int lda, long long strideA,

@@ -48,6 +48,17 @@ constexpr int kMaxDevices = 64;
 DeviceInfo g_dev[kMaxDevices];
 std::mutex g_dev_mu;
 
+// host-buffer entry: per-device internal streams and a grow-only workspace
+struct HostCtx {
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    float* ws = nullptr;
+    size_t ws_bytes = 0;
+};
+HostCtx g_host[kMaxDevices];
+
 emu_status device_check(int& dev, int& sms)
 {
     if (cudaGetDevice(&dev) != cudaSuccess) return EMU_STATUS_CUDA_ERROR;
@@ -333,63 +344,110 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_host(int m, 
     if (st != EMU_STATUS_SUCCESS) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
 
-    // device buffers mirror the host layout of one chunk of problems; only the
-    // m x k / k x n / m x n parts are copied (2-D copies), gaps are left alone
+    // Problems are processed in chunks on two internal streams: the host->device
+    // copy of chunk c+1 and the device->host copy of chunk c-1 overlap the kernel
+    // of chunk c.  Device buffers mirror the host layout of one chunk; only the
+    // m x k / k x n / m x n parts are copied (2-D copies), gaps are left alone.
+    HostCtx& hc = g_host[dev];
+    std::lock_guard<std::mutex> lk(hc.mu);
+    if (!hc.init) {
+        if (cudaStreamCreateWithFlags(&hc.st[0], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&hc.st[1], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&hc.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&hc.join[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&hc.join[1], cudaEventDisableTiming) != cudaSuccess)
+            return EMU_STATUS_CUDA_ERROR;
+        hc.init = true;
+    }
     auto span = [](long long ld, long long cols, long long rows, long long stride, int nb) {
         return (long long)(nb - 1) * stride + ld * (cols - 1) + rows;
     };
-    auto copy = [&](float* dst, const float* src, long long ld, long long cols, long long rows, long long stride,
-                    int nb, cudaMemcpyKind kind) -> bool {
+    auto copy = [](float* dst, const float* src, long long ld, long long cols, long long rows, long long stride, int nb,
+                   cudaMemcpyKind kind, cudaStream_t cs) -> bool {
         if (nb == 1 || stride == ld * cols) {
-            const long long h = (nb == 1 ? 1 : nb) * cols;
+            const long long h = (long long)nb * cols;
             if (ld == rows)   // contiguous: one linear copy
-                return cudaMemcpyAsync(dst, src, (size_t)(h * rows * 4), kind, s) == cudaSuccess;
-            return cudaMemcpy2DAsync(dst, ld * 4, src, ld * 4, rows * 4, h, kind, s) == cudaSuccess;
+                return cudaMemcpyAsync(dst, src, (size_t)(h * rows * 4), kind, cs) == cudaSuccess;
+            return cudaMemcpy2DAsync(dst, ld * 4, src, ld * 4, rows * 4, h, kind, cs) == cudaSuccess;
         }
         for (int i = 0; i < nb; ++i)
-            if (cudaMemcpy2DAsync(dst + i * stride, ld * 4, src + i * stride, ld * 4, rows * 4, cols, kind, s) !=
+            if (cudaMemcpy2DAsync(dst + i * stride, ld * 4, src + i * stride, ld * 4, rows * 4, cols, kind, cs) !=
                 cudaSuccess)
                 return false;
         return true;
     };
-    const int per = batch;
-    const long long spanA = reads_ab ? span(lda, k, m, strideA, per) : 0;
-    const long long spanB = reads_ab ? span(ldb, n, k, strideB, per) : 0;
+    const int nchunks = batch >= 16 ? 8 : 1;
+    const int per = (batch + nchunks - 1) / nchunks;
+    const bool shA = strideA == 0 || batch == 1, shB = strideB == 0 || batch == 1;
+    const long long spanA = reads_ab ? span(lda, k, m, shA ? 0 : strideA, shA ? 1 : per) : 0;
+    const long long spanB = reads_ab ? span(ldb, n, k, shB ? 0 : strideB, shB ? 1 : per) : 0;
     const long long spanC = span(ldc, n, m, strideC, per);
-    float *dA = nullptr, *dB = nullptr, *dC = nullptr;
-    if (reads_ab) {
-        if (cudaMallocAsync((void**)&dA, sizeof(float) * spanA, s) != cudaSuccess) return EMU_STATUS_CUDA_ERROR;
-        if (cudaMallocAsync((void**)&dB, sizeof(float) * spanB, s) != cudaSuccess) {
-            cudaFreeAsync(dA, s);
-            return EMU_STATUS_CUDA_ERROR;
-        }
+    const int nslot = nchunks > 1 ? 2 : 1;
+    const size_t need = sizeof(float) * (size_t)((shA ? spanA : nslot * spanA) + (shB ? spanB : nslot * spanB) +
+                                                 nslot * spanC + 64);
+    if (hc.ws_bytes < need) {
+        if (hc.ws) cudaFree(hc.ws);
+        hc.ws = nullptr;
+        hc.ws_bytes = 0;
+        if (cudaMalloc((void**)&hc.ws, need) != cudaSuccess) return EMU_STATUS_CUDA_ERROR;
+        hc.ws_bytes = need;
     }
-    if (cudaMallocAsync((void**)&dC, sizeof(float) * spanC, s) != cudaSuccess) {
-        if (dA) cudaFreeAsync(dA, s);
-        if (dB) cudaFreeAsync(dB, s);
-        return EMU_STATUS_CUDA_ERROR;
+    auto align16f = [](float* q) { return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q) + 15) & ~uintptr_t(15)); };
+    float* cur = hc.ws;
+    float* dA = cur; cur = align16f(cur + (shA ? spanA : nslot * spanA));
+    float* dB = cur; cur = align16f(cur + (shB ? spanB : nslot * spanB));
+    float* dC = cur;
+    bool ok = cudaEventRecord(hc.fork, s) == cudaSuccess && cudaStreamWaitEvent(hc.st[0], hc.fork, 0) == cudaSuccess &&
+              cudaStreamWaitEvent(hc.st[1], hc.fork, 0) == cudaSuccess;
+    if (ok && reads_ab && shA) ok = copy(dA, A, lda, k, m, 0, 1, cudaMemcpyHostToDevice, hc.st[0]);
+    if (ok && reads_ab && shB) ok = copy(dB, B, ldb, n, k, 0, 1, cudaMemcpyHostToDevice, hc.st[0]);
+    if (ok && nslot > 1 && (shA || shB)) {   // stream 1 must see the shared operands
+        ok = cudaEventRecord(hc.join[0], hc.st[0]) == cudaSuccess &&
+             cudaStreamWaitEvent(hc.st[1], hc.join[0], 0) == cudaSuccess;
     }
     int launches = 0;
-    bool ok = true;
-    if (reads_ab) {
-        ok = ok && copy(dA, A, lda, k, m, strideA, strideA == 0 ? 1 : batch, cudaMemcpyHostToDevice);
-        ok = ok && copy(dB, B, ldb, n, k, strideB, strideB == 0 ? 1 : batch, cudaMemcpyHostToDevice);
-    }
-    if (beta != 0.0f) ok = ok && copy(dC, C, ldc, n, m, strideC, batch, cudaMemcpyHostToDevice);
-    if (!ok) st = EMU_STATUS_CUDA_ERROR;
-    if (st == EMU_STATUS_SUCCESS) {
-        st = emu_sgemm_batched_ex(m, n, k, alpha, dA, lda, strideA, dB, ldb, strideB, beta, dC, ldc, strideC, batch,
-                                  mode, stream, nullptr, 0, 0u);
+    for (int c = 0; c < nchunks && ok && st == EMU_STATUS_SUCCESS; ++c) {
+        const int b0 = c * per;
+        const int nb = std::min(per, batch - b0);
+        if (nb <= 0) break;
+        const int slot = c % nslot;
+        cudaStream_t cs = hc.st[slot];
+        float* a = shA ? dA : dA + slot * spanA;
+        float* bb = shB ? dB : dB + slot * spanB;
+        float* cc = dC + slot * spanC;
+        if (reads_ab && !shA) ok = ok && copy(a, A + (long long)b0 * strideA, lda, k, m, strideA, nb, cudaMemcpyHostToDevice, cs);
+        if (reads_ab && !shB) ok = ok && copy(bb, B + (long long)b0 * strideB, ldb, n, k, strideB, nb, cudaMemcpyHostToDevice, cs);
+        if (beta != 0.0f) ok = ok && copy(cc, C + (long long)b0 * strideC, ldc, n, m, strideC, nb, cudaMemcpyHostToDevice, cs);
+        if (!ok) break;
+        st = emu_sgemm_batched_ex(m, n, k, alpha, reads_ab ? a : nullptr, lda, shA ? 0 : strideA,
+                                  reads_ab ? bb : nullptr, ldb, shB ? 0 : strideB, beta, cc, ldc, strideC, nb, mode,
+                                  cs, nullptr, 0, 0u);
         launches += g_last_launches;
+        if (st == EMU_STATUS_SUCCESS)
+            ok = copy(C + (long long)b0 * strideC, cc, ldc, n, m, strideC, nb, cudaMemcpyDeviceToHost, cs);
     }
-    if (st == EMU_STATUS_SUCCESS && !copy(C, dC, ldc, n, m, strideC, batch, cudaMemcpyDeviceToHost))
-        st = EMU_STATUS_CUDA_ERROR;
-    if (dA) cudaFreeAsync(dA, s);
-    if (dB) cudaFreeAsync(dB, s);
-    cudaFreeAsync(dC, s);
+    for (int i = 0; i < nslot; ++i) {
+        cudaEventRecord(hc.join[i], hc.st[i]);
+        cudaStreamWaitEvent(s, hc.join[i], 0);
+    }
+    if (!ok && st == EMU_STATUS_SUCCESS) st = EMU_STATUS_CUDA_ERROR;
     if (cudaStreamSynchronize(s) != cudaSuccess && st == EMU_STATUS_SUCCESS) st = EMU_STATUS_CUDA_ERROR;
     g_last_launches = launches;
     return st;
 }
+
+#ifdef EMU_PROF
+// profiling build only (tools/prof_roles.py): read and reset the role counters
+__attribute__((visibility("default"))) int emu_prof_read(unsigned long long* host, int n)
+{
+    cudaDeviceSynchronize();
+    return cudaMemcpyFromSymbol(host, emu::g_prof, sizeof(unsigned long long) * (n < 16 ? n : 16)) == cudaSuccess ? 0 : 1;
+}
+__attribute__((visibility("default"))) int emu_prof_reset(void)
+{
+    unsigned long long z[16] = {};
+    return cudaMemcpyToSymbol(emu::g_prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 }  // extern "C"

@@ -44,6 +44,28 @@
 
 namespace emu {
 
+// Optional role timing (build with -DEMU_PROF; tools/ only, never the product
+// library): lane 0 of each role warp accumulates clock64() cycles per event.
+#ifdef EMU_PROF
+enum ProfSlot { P_PROD_WAIT_EMPTY, P_MMA_WAIT_ACC, P_MMA_WAIT_OP, P_SPL_WAIT_F32, P_SPL_WAIT_OP, P_SPL_WORK,
+                P_EPI_WAIT_ACC, P_EPI_DRAIN, P_EPI_STORE, P_CTA_TOTAL, P_MMA_ISSUE, P_NSLOTS };
+__device__ unsigned long long g_prof[16];
+#define PROF_DECL unsigned long long prof_acc[P_NSLOTS] = {}; long long prof_t0 = 0;
+#define PROF_T0() (prof_t0 = clock64())
+#define PROF_ADD(slot) (prof_acc[slot] += (unsigned long long)(clock64() - prof_t0))
+#define PROF_FLUSH()                                                            \
+    do {                                                                        \
+        if ((threadIdx.x & 31) == 0)                                            \
+            for (int i_ = 0; i_ < P_NSLOTS; ++i_)                               \
+                if (prof_acc[i_]) atomicAdd(&g_prof[i_], prof_acc[i_]);         \
+    } while (0)
+#else
+#define PROF_DECL
+#define PROF_T0() ((void)0)
+#define PROF_ADD(slot) ((void)0)
+#define PROF_FLUSH() ((void)0)
+#endif
+
 struct GemmParams {
     int m, n, k;
     int a_batched, b_batched;     // 0: batch coordinate 0 for every problem (stride 0)
@@ -160,6 +182,10 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
+    PROF_DECL
+#ifdef EMU_PROF
+    const long long prof_start = clock64();
+#endif
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < Cfg::S32; ++i) {
@@ -197,7 +223,9 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 tile_coords(p, t, b, mt, nt);
                 const int ab = p.a_batched ? b : 0, bb = p.b_batched ? b : 0;
                 for (int ks = 0; ks < nks; ++ks) {
+                    PROF_T0();
                     ptx::mbar_wait_sleep(&f32_empty[s], ph ^ 1);
+                    PROF_ADD(P_PROD_WAIT_EMPTY);
                     uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                     ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
                     ptx::tma_load_3d(dst, &tmA, &f32_full[s], mt * Cfg::BM, ks * Cfg::BK, ab, pol);
@@ -214,14 +242,19 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
                 for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                     const uint32_t buf = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+                    PROF_T0();
                     ptx::mbar_wait(&acc_empty[buf], aph ^ 1);
+                    PROF_ADD(P_MMA_WAIT_ACC);
                     ptx::tc_fence_after();
                     const uint32_t d_hi = tmem_base + buf * 2 * BN;
                     const uint32_t d_corr = d_hi + BN;
                     const int ks0 = kb * p.kb_stages;
                     const int ks1 = min(ks0 + p.kb_stages, nks);
                     for (int ks = ks0; ks < ks1; ++ks) {
+                        PROF_T0();
                         ptx::mbar_wait(&op_full[s], ph);
+                        PROF_ADD(P_MMA_WAIT_OP);
+                        PROF_T0();
                         ptx::tc_fence_after();
                         const uint32_t base = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
                         const uint32_t a_hi = base, a_lo = base + Cfg::AOP_BYTES;
@@ -251,6 +284,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             }
                         }
                         ptx::tc_commit(&op_empty[s]);   // operand stage free when these MMAs finish
+                        PROF_ADD(P_MMA_ISSUE);
                         if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                     }
                     ptx::tc_commit(&acc_full[buf]);     // k-block accumulators ready
@@ -270,8 +304,13 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const float* gA = LDG ? p.A + (long long)tb * p.strideA : nullptr;
             const float* gB = LDG ? p.B + (long long)tb * p.strideB : nullptr;
             for (int ks = 0; ks < nks; ++ks) {
+                PROF_T0();
                 if (!LDG) ptx::mbar_wait(&f32_full[s32], ph32);
+                PROF_ADD(P_SPL_WAIT_F32);
+                PROF_T0();
                 ptx::mbar_wait(&op_empty[sop], phop ^ 1);
+                PROF_ADD(P_SPL_WAIT_OP);
+                PROF_T0();
                 const uint8_t* fa = f32buf + s32 * Cfg::F32_STAGE;
                 const uint8_t* fb = fa + Cfg::A32_BYTES;
                 const int m0 = tmt * Cfg::BM, n0 = tnt * BN, k0 = ks * Cfg::BK;
@@ -386,6 +425,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                 }
                 ptx::fence_proxy_async_smem();        // our st.shared -> visible to UMMA
+                PROF_ADD(P_SPL_WORK);
                 ptx::mbar_arrive(&op_full[sop]);
                 if (!LDG) ptx::mbar_arrive(&f32_empty[s32]);
                 if (++s32 == Cfg::S32) { s32 = 0; ph32 ^= 1; }
@@ -412,7 +452,10 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
             for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                 const uint32_t buf = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+                PROF_T0();
                 ptx::mbar_wait_sleep(&acc_full[buf], aph);
+                PROF_ADD(P_EPI_WAIT_ACC);
+                PROF_T0();
                 ptx::tc_fence_after();
                 const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * BN + h * HALF;
 #pragma unroll
@@ -429,7 +472,9 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&acc_empty[buf]);
+                PROF_ADD(P_EPI_DRAIN);
             }
+            PROF_T0();
             // epilogue: C = RN(alpha*C + RN(beta*C_old)), column-major, coalesced per column
             const int r = mt * Cfg::BM + (int)(q * 32 + lane);
             const int col0 = nt * BN + (int)(h * HALF);
@@ -448,8 +493,15 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         if (col0 + j < p.n) cp[(long long)j * p.ldc] = fmaf(p.alpha, creg[j], 0.0f);
                 }
             }
+            PROF_ADD(P_EPI_STORE);
         }
     }
+#ifdef EMU_PROF
+    if (warp >= 2 || lane == 0) {   // role warps (and the elected lanes of warps 0, 1)
+        prof_acc[P_CTA_TOTAL] = (warp == 2 && lane == 0) ? (unsigned long long)(clock64() - prof_start) : 0;
+        PROF_FLUSH();
+    }
+#endif
 
     ptx::tc_fence_before();
     __syncthreads();

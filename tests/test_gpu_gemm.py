@@ -154,7 +154,7 @@ def test_deterministic(mode):
     C1 = emu_gpu(mode, A, B, m, n, k)
     C2 = emu_gpu(mode, A, B, m, n, k)
     assert np.array_equal(C1, C2)
-    # batch-sharded halves == the whole (the multi-GPU partition, R#20)
+    # batch-sharded halves == the whole (the multi-GPU partition, R#21)
     Ch = np.concatenate([emu_gpu(mode, A[:2], B[:2], m, n, k), emu_gpu(mode, A[2:], B[2:], m, n, k)])
     assert np.array_equal(C1, Ch)
 
