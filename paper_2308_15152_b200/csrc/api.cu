@@ -150,6 +150,8 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, long long count, 
     }
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 emu_status launch_status(cudaError_t e)
 {
     if (e == cudaSuccess) return EMU_STATUS_SUCCESS;
@@ -168,9 +170,20 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
 
     const bool a_b = batch > 1 && strideA != 0;
     const bool b_b = batch > 1 && strideB != 0;
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmC;
     std::memset(&tmA, 0, sizeof(tmA));
     std::memset(&tmB, 0, sizeof(tmB));
+    std::memset(&tmC, 0, sizeof(tmC));
+    // TMA-store epilogue: beta == 0 and a 16-byte-unit C layout
+    const bool c_b = batch > 1;
+    int tma_store = Cfg::CSTAGE_BYTES != 0 && beta == 0.0f && aligned16(C) && ldc % 4 == 0 &&
+                    (!c_b || strideC % 4 == 0) && (unsigned long long)strideC * 4 < (1ull << 40);
+    if (tma_store) {
+        const uint64_t sC = c_b ? (uint64_t)strideC : (((uint64_t)ldc * (uint64_t)n + 3) & ~uint64_t(3));
+        if (!make_map(&tmC, C, (uint64_t)m, (uint64_t)n, (uint64_t)ldc, c_b ? (uint64_t)batch : 1, sC, Cfg::BM, 32,
+                      CU_TENSOR_MAP_SWIZZLE_NONE))
+            tma_store = 0;
+    }
     // dim-2 stride: any valid value when the batch extent is 1
     const uint64_t sA = a_b ? (uint64_t)strideA : (((uint64_t)lda * (uint64_t)k + 3) & ~uint64_t(3));
     const uint64_t sB = b_b ? (uint64_t)strideB : (((uint64_t)ldb * (uint64_t)n + 3) & ~uint64_t(3));
@@ -193,16 +206,15 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     p.kb_stages = (kblock > 0 ? kblock : 64) / Cfg::BK;
     p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
     p.range_flag = MODE == 0 ? range_flag : nullptr;
+    p.tma_store = tma_store;
     p.A = A; p.B = B; p.lda = lda; p.ldb = ldb;
     p.strideA = a_b ? strideA : 0; p.strideB = b_b ? strideB : 0;
 
     const long long grid = std::min<long long>(p.num_tiles, sms);
-    emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE, LDG><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, p);
+    emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE, LDG><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
 }
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
 

@@ -77,6 +77,7 @@ struct GemmParams {
     int num_k_stages;             // ceil(k / 32)
     int kb_stages;                // KB / 32
     int corr;                     // 1 = the paper's method; 0 = "correction off" control
+    int tma_store;                // 1: epilogue stages C in shared memory and TMA-stores it (beta == 0)
     unsigned int* range_flag;     // nullable (FP16 mode only)
     // direct-load (LDG) variant only: operands read by the splitter warps
     const float* A;
@@ -105,7 +106,10 @@ struct GemmCfg {
     static constexpr uint32_t BOP_BYTES = BN * BK * ESZ;
     static constexpr uint32_t OP_STAGE = 2 * AOP_BYTES + 2 * BOP_BYTES;
     static constexpr int S32 = MODE == 0 ? 3 : 2;
-    static constexpr int SOP = MODE == 0 ? 3 : 2;
+    static constexpr int SOP = 2;
+    // C staging tile for the TMA-store epilogue (FP16 mode; TF32's operand ring
+    // leaves no room, it stores with STG)
+    static constexpr uint32_t CSTAGE_BYTES = MODE == 0 ? BM * BN * 4 : 0;
     static constexpr uint32_t B_ROW = BK * ESZ;         // 64 (FP16) or 128 (TF32)
     static constexpr uint32_t B_SBO = 8 * B_ROW;
     static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;  // SW64 / SW128
@@ -121,7 +125,7 @@ struct GemmCfg {
     static constexpr uint32_t A_MAJOR = ALAY == A_K_SW128 ? 0 : 1;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
-    static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + BAR_BYTES;
+    static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + CSTAGE_BYTES + BAR_BYTES;
     static constexpr int SPLIT_WARP0 = 2, NUM_SPLIT_WARPS = 8;
     static constexpr int EPI_WARP0 = 10, NUM_EPI_WARPS = 8;
     static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
@@ -162,7 +166,7 @@ __device__ __forceinline__ void split4_fp16(const float4 v, uint2& h, uint2& l)
 template <int MODE, int BN, int ALAY, bool RANGE, bool LDG>
 __global__ void __launch_bounds__(GemmCfg<MODE, BN, ALAY>::NUM_THREADS, 1)
 emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const GemmParams p)
+                 const __grid_constant__ CUtensorMap tmC, const GemmParams p)
 {
     using Cfg = GemmCfg<MODE, BN, ALAY>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -171,7 +175,8 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* f32buf = smem;
     uint8_t* opbuf = smem + Cfg::S32 * Cfg::F32_STAGE;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(opbuf + Cfg::SOP * Cfg::OP_STAGE);
+    float* cstage = reinterpret_cast<float*>(opbuf + Cfg::SOP * Cfg::OP_STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(opbuf + Cfg::SOP * Cfg::OP_STAGE + Cfg::CSTAGE_BYTES);
     uint64_t* f32_full = bars;
     uint64_t* f32_empty = f32_full + Cfg::S32;
     uint64_t* op_full = f32_empty + Cfg::S32;
@@ -216,7 +221,20 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (!LDG && ptx::elect_one()) {
-            const uint64_t pol = ptx::l2_policy_evict_last();
+            // L2 prefetch cursor PF stages ahead of the loads: deepens the memory
+            // pipeline beyond the S32 shared-memory stages (the loads then hit L2)
+            constexpr int PF = 8;
+            long long pt = blockIdx.x;
+            int pks = 0;
+            auto prefetch_next = [&]() {
+                if (pt >= p.num_tiles) return;
+                int b, mt, nt;
+                tile_coords(p, pt, b, mt, nt);
+                ptx::tma_prefetch_3d(&tmA, mt * Cfg::BM, pks * Cfg::BK, p.a_batched ? b : 0);
+                ptx::tma_prefetch_3d(&tmB, pks * Cfg::BK, nt * BN, p.b_batched ? b : 0);
+                if (++pks == nks) { pks = 0; pt += gridDim.x; }
+            };
+            for (int i = 0; i < PF; ++i) prefetch_next();
             uint32_t s = 0, ph = 0;
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
                 int b, mt, nt;
@@ -228,8 +246,9 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     PROF_ADD(P_PROD_WAIT_EMPTY);
                     uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                     ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
-                    ptx::tma_load_3d(dst, &tmA, &f32_full[s], mt * Cfg::BM, ks * Cfg::BK, ab, pol);
-                    ptx::tma_load_3d(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK, nt * BN, bb, pol);
+                    ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * Cfg::BM, ks * Cfg::BK, ab);
+                    ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK, nt * BN, bb);
+                    prefetch_next();
                     if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                 }
             }
@@ -342,26 +361,46 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 uint8_t* oa_lo = o + Cfg::AOP_BYTES;
                 uint8_t* ob_hi = o + 2 * Cfg::AOP_BYTES;
                 uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
+                // ---- load phase: every FP32 value this thread splits in this stage is
+                // read before the first store (the stores cannot alias the loads, but
+                // the compiler cannot prove it and would serialise load -> store)
+                float4 va[4], vb[4];
+                const uint32_t n = row;
                 if (ALAY == A_K_SW128) {
                     // A K-major (TF32): thread = (m row, 16-k half); 4 k per 16-byte chunk
 #pragma unroll
                     for (int jj = 0; jj < 4; ++jj) {
+                        const uint32_t k4 = 4 * (half * 4 + jj);
+                        va[jj] = make_float4(a1(row, k4), a1(row, k4 + 1), a1(row, k4 + 2), a1(row, k4 + 3));
+                    }
+                } else {
+                    // A MN-major: warp sw handles k rows sw, sw+8, ...; lane handles m = 4*lane .. +3
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) va[kk] = a4(lane * 4, sw + 8 * kk);
+                }
+                // B: thread = (n row, 16-k half): 4 chunks of 4 k
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) vb[jj] = b4(n, half * 4 + jj);
+
+                // ---- split + store phase
+                if (ALAY == A_K_SW128) {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
                         const uint32_t j = half * 4 + jj;
                         uint4 hv, lv;
-                        split_tf32(a1(row, 4 * j), hv.x, lv.x);
-                        split_tf32(a1(row, 4 * j + 1), hv.y, lv.y);
-                        split_tf32(a1(row, 4 * j + 2), hv.z, lv.z);
-                        split_tf32(a1(row, 4 * j + 3), hv.w, lv.w);
+                        split_tf32(va[jj].x, hv.x, lv.x);
+                        split_tf32(va[jj].y, hv.y, lv.y);
+                        split_tf32(va[jj].z, hv.z, lv.z);
+                        split_tf32(va[jj].w, hv.w, lv.w);
                         const uint32_t off = row * Cfg::B_ROW + ((j ^ (row & 7)) << 4);
                         *reinterpret_cast<uint4*>(oa_hi + off) = hv;
                         *reinterpret_cast<uint4*>(oa_lo + off) = lv;
                     }
                 } else {
-                    // A MN-major: warp sw handles k rows sw, sw+8, ...; lane handles m = 4*lane .. +3
 #pragma unroll
-                    for (int kk = 0; kk < Cfg::BK / 8; ++kk) {
+                    for (int kk = 0; kk < 4; ++kk) {
                         const uint32_t k = sw + 8 * kk;
-                        const float4 v = a4(lane * 4, k);
+                        const float4 v = va[kk];
                         if (MODE == 0) {
                             const uint32_t g = k >> 3, kr = k & 7;
                             uint2 h, l;
@@ -389,39 +428,33 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         }
                     }
                 }
-                // B: thread = (n row, 16-k half)
-                {
-                    const uint32_t n = row;
-                    if (MODE == 0) {
+                if (MODE == 0) {
 #pragma unroll
-                        for (int jj = 0; jj < 2; ++jj) {   // 8 k per 16-byte FP16 chunk
-                            const uint32_t j = half * 2 + jj;
-                            const float4 v0 = b4(n, 2 * j);
-                            const float4 v1 = b4(n, 2 * j + 1);
-                            uint2 h0, l0, h1, l1;
-                            split4_fp16(v0, h0, l0);
-                            split4_fp16(v1, h1, l1);
-                            if (RANGE)
-                                nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) |
-                                             f16x2_nonfinite(h1.x) | f16x2_nonfinite(h1.y);
-                            const uint32_t off = n * 64 + ((j ^ ((n >> 1) & 3)) << 4);
-                            *reinterpret_cast<uint4*>(ob_hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
-                            *reinterpret_cast<uint4*>(ob_lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
-                        }
-                    } else {
+                    for (int jj = 0; jj < 2; ++jj) {   // 8 k per 16-byte FP16 chunk
+                        const uint32_t j = half * 2 + jj;
+                        uint2 h0, l0, h1, l1;
+                        split4_fp16(vb[2 * jj], h0, l0);
+                        split4_fp16(vb[2 * jj + 1], h1, l1);
+                        if (RANGE)
+                            nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) |
+                                         f16x2_nonfinite(h1.x) | f16x2_nonfinite(h1.y);
+                        const uint32_t off = n * 64 + ((j ^ ((n >> 1) & 3)) << 4);
+                        *reinterpret_cast<uint4*>(ob_hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+                        *reinterpret_cast<uint4*>(ob_lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+                    }
+                } else {
 #pragma unroll
-                        for (int jj = 0; jj < 4; ++jj) {   // 4 k per 16-byte TF32 chunk
-                            const uint32_t j = half * 4 + jj;
-                            const float4 v = b4(n, j);
-                            uint4 h, l;
-                            split_tf32(v.x, h.x, l.x);
-                            split_tf32(v.y, h.y, l.y);
-                            split_tf32(v.z, h.z, l.z);
-                            split_tf32(v.w, h.w, l.w);
-                            const uint32_t off = n * 128 + ((j ^ (n & 7)) << 4);
-                            *reinterpret_cast<uint4*>(ob_hi + off) = h;
-                            *reinterpret_cast<uint4*>(ob_lo + off) = l;
-                        }
+                    for (int jj = 0; jj < 4; ++jj) {   // 4 k per 16-byte TF32 chunk
+                        const uint32_t j = half * 4 + jj;
+                        const float4 v = vb[jj];
+                        uint4 h, l;
+                        split_tf32(v.x, h.x, l.x);
+                        split_tf32(v.y, h.y, l.y);
+                        split_tf32(v.z, h.z, l.z);
+                        split_tf32(v.w, h.w, l.w);
+                        const uint32_t off = n * 128 + ((j ^ (n & 7)) << 4);
+                        *reinterpret_cast<uint4*>(ob_hi + off) = h;
+                        *reinterpret_cast<uint4*>(ob_lo + off) = l;
                     }
                 }
                 ptx::fence_proxy_async_smem();        // our st.shared -> visible to UMMA
@@ -475,26 +508,50 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 PROF_ADD(P_EPI_DRAIN);
             }
             PROF_T0();
-            // epilogue: C = RN(alpha*C + RN(beta*C_old)), column-major, coalesced per column
-            const int r = mt * Cfg::BM + (int)(q * 32 + lane);
-            const int col0 = nt * BN + (int)(h * HALF);
-            if (r < p.m) {
-                float* cp = p.C + (long long)b * p.strideC + r + (long long)col0 * p.ldc;
-                if (p.beta != 0.0f) {
+            // epilogue: C = RN(alpha*C + RN(beta*C_old)), column-major
+            if (Cfg::CSTAGE_BYTES != 0 && p.tma_store) {
+                // beta == 0: stage the tile in shared memory ([n][m], 512-byte
+                // columns; a warp writes 32 consecutive m -> conflict-free) and let
+                // one thread TMA-store it, so these warps go straight back to
+                // draining the next tile while the stores stream out.
+                const bool leader = (e == 0 && lane == 0);
+                if (leader) ptx::bulk_wait_group_read0();       // previous tile's store has read the stage
+                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                const uint32_t r = q * 32 + lane;
 #pragma unroll
-                    for (int j = 0; j < HALF; ++j)
-                        if (col0 + j < p.n) {
-                            float* dst = cp + (long long)j * p.ldc;
-                            *dst = fmaf(p.alpha, creg[j], __fmul_rn(p.beta, *dst));
-                        }
-                } else {
+                for (int j = 0; j < HALF; ++j)
+                    cstage[(h * HALF + j) * Cfg::BM + r] = fmaf(p.alpha, creg[j], 0.0f);
+                ptx::fence_proxy_async_smem();
+                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                if (leader) {
 #pragma unroll
-                    for (int j = 0; j < HALF; ++j)
-                        if (col0 + j < p.n) cp[(long long)j * p.ldc] = fmaf(p.alpha, creg[j], 0.0f);
+                    for (int c = 0; c < BN / 32; ++c)
+                        ptx::tma_store_3d(&tmC, cstage + c * 32 * Cfg::BM, mt * Cfg::BM, nt * BN + c * 32, b);
+                    ptx::bulk_commit_group();
+                }
+            } else {
+                const int r = mt * Cfg::BM + (int)(q * 32 + lane);
+                const int col0 = nt * BN + (int)(h * HALF);
+                if (r < p.m) {
+                    float* cp = p.C + (long long)b * p.strideC + r + (long long)col0 * p.ldc;
+                    if (p.beta != 0.0f) {
+#pragma unroll
+                        for (int j = 0; j < HALF; ++j)
+                            if (col0 + j < p.n) {
+                                float* dst = cp + (long long)j * p.ldc;
+                                *dst = fmaf(p.alpha, creg[j], __fmul_rn(p.beta, *dst));
+                            }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < HALF; ++j)
+                            if (col0 + j < p.n) cp[(long long)j * p.ldc] = fmaf(p.alpha, creg[j], 0.0f);
+                    }
                 }
             }
             PROF_ADD(P_EPI_STORE);
         }
+        if (Cfg::CSTAGE_BYTES != 0 && p.tma_store && warp == Cfg::EPI_WARP0 && lane == 0)
+            ptx::bulk_wait_group0();   // global writes complete before the CTA retires
     }
 #ifdef EMU_PROF
     if (warp >= 2 || lane == 0) {   // role warps (and the elected lanes of warps 0, 1)

@@ -1,0 +1,14 @@
+#!/bin/bash
+# quick iteration: build, correctness subset, benches, role profile.  bash tools/gpu_iter.sh TAG
+TAG=${1:-it}
+mkdir -p gpurun_out
+python paper_2308_15152_b200/build.py > gpurun_out/build_$TAG.log 2>&1 || { echo BUILD FAILED; exit 1; }
+python -c "import oracle; oracle.build()"
+timeout 300 python tools/dbg_small.py > gpurun_out/dbg_$TAG.log 2>&1; echo "dbg rc=$?" >> gpurun_out/dbg_$TAG.log
+timeout 900 python -m pytest tests/test_gpu_gemm.py -q -x > gpurun_out/pytest_gemm_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gemm_$TAG.log
+for mode in fp16 tf32; do
+  timeout 300 python bench.py --steps 200 --warmup 10 --mode $mode --no-cpu-baseline --no-e2e > gpurun_out/bench_c2_${mode}_$TAG.log 2>&1
+  timeout 300 python bench.py --steps 5 --warmup 3 --mode $mode --config c3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_${mode}_$TAG.log 2>&1
+done
+rm -f gpurun_out/prof_roles_$TAG.log
+for c in c2 c3; do for md in fp16 tf32; do timeout 300 python tools/prof_roles.py $c $md 3 >> gpurun_out/prof_roles_$TAG.log 2>&1; done; done

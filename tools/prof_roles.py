@@ -21,7 +21,9 @@ SLOTS = ["prod_wait_empty", "mma_wait_acc", "mma_wait_op", "spl_wait_f32", "spl_
 
 
 def build():
-    flags = [f for f in B.FLAGS if f != "-v"]
+    flags = list(B.FLAGS)
+    i = flags.index("-Xptxas")
+    del flags[i:i + 2]
     cmd = [B.NVCC, *flags, "-DEMU_PROF", "-o", LIB, *B.SOURCES]
     subprocess.check_call(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
 
