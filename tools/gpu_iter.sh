@@ -4,7 +4,8 @@ TAG=${1:-it}
 mkdir -p gpurun_out
 python paper_2308_15152_b200/build.py > gpurun_out/build_$TAG.log 2>&1 || { echo BUILD FAILED; exit 1; }
 python -c "import oracle; oracle.build()"
-timeout 300 python tools/dbg_small.py > gpurun_out/dbg_$TAG.log 2>&1; echo "dbg rc=$?" >> gpurun_out/dbg_$TAG.log
+timeout 120 python tools/dbg_small.py > gpurun_out/dbg_$TAG.log 2>&1; RC=$?; echo "dbg rc=$RC" >> gpurun_out/dbg_$TAG.log
+if [ $RC -ne 0 ]; then echo "dbg failed rc=$RC"; exit 1; fi
 timeout 900 python -m pytest tests/test_gpu_gemm.py -q -x > gpurun_out/pytest_gemm_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gemm_$TAG.log
 for mode in fp16 tf32; do
   timeout 300 python bench.py --steps 200 --warmup 10 --mode $mode --no-cpu-baseline --no-e2e > gpurun_out/bench_c2_${mode}_$TAG.log 2>&1
