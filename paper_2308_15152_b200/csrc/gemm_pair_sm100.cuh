@@ -44,9 +44,12 @@ struct PairCfg {
     static constexpr uint32_t AOP_BYTES = BM * BK * ESZ;
     static constexpr uint32_t BOP_BYTES = BNC * BK * ESZ;
     static constexpr uint32_t OP_STAGE = 2 * AOP_BYTES + 2 * BOP_BYTES;
-    static constexpr int S32 = MODE == 0 ? 4 : 2;
+    static constexpr int S32 = MODE == 0 ? 4 : 3;
     static constexpr int SOP = 2;
-    static constexpr uint32_t CSTAGE_BYTES = BM * BN * 4;  // 64 KB: TMA-store staging
+    // TMA-store staging: the whole C tile (FP16 mode, 64 KB) or half of it (TF32,
+    // 32 KB; the two column halves are staged and stored one after the other)
+    static constexpr int CSTAGE_PARTS = MODE == 0 ? 1 : 2;
+    static constexpr uint32_t CSTAGE_BYTES = BM * (BN / CSTAGE_PARTS) * 4;
     static constexpr uint32_t B_ROW = BK * ESZ;
     static constexpr uint32_t B_SBO = 8 * B_ROW;
     static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;
@@ -359,10 +362,13 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                     ptx::tmem_ld8(taddr + c * 8, vh);
                     ptx::tmem_ld8(taddr + Cfg::BN + c * 8, vc);
                     ptx::tmem_wait_ld();
+                    if (p.corr) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float tt = p.corr ? fmaf(vc[j], scale, vh[j]) : vh[j];
-                        creg[c * 8 + j] = __fadd_rn(creg[c * 8 + j], tt);
+                        for (int j = 0; j < 8; j += 2)
+                            combine2(creg[c * 8 + j], creg[c * 8 + j + 1], vh[j], vh[j + 1], vc[j], vc[j + 1], scale);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) creg[c * 8 + j] = __fadd_rn(creg[c * 8 + j], vh[j]);
                     }
                 }
                 ptx::tc_fence_before();
@@ -373,20 +379,27 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
             PROF_T0();
             const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
             if (p.tma_store) {
+                // stage the C tile (in CSTAGE_PARTS column parts) and TMA-store it
                 const bool leader = (e == 0 && lane == 0);
-                if (leader) ptx::bulk_wait_group_read0();
-                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
                 const uint32_t r = q * 32 + lane;
+                constexpr int PART = Cfg::BN / Cfg::CSTAGE_PARTS;
 #pragma unroll
-                for (int j = 0; j < HALF; ++j)
-                    cstage[(h * HALF + j) * Cfg::BM + r] = fmaf(p.alpha, creg[j], 0.0f);
-                ptx::fence_proxy_async_smem();
-                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
-                if (leader) {
+                for (int part = 0; part < Cfg::CSTAGE_PARTS; ++part) {
+                    if (leader) ptx::bulk_wait_group_read0();   // staging buffer free
+                    ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                    if (Cfg::CSTAGE_PARTS == 1 || h == (uint32_t)part) {
+                        float* dst = cstage + (Cfg::CSTAGE_PARTS == 1 ? h * HALF * Cfg::BM : 0);
 #pragma unroll
-                    for (int c = 0; c < Cfg::BN / 32; ++c)
-                        ptx::tma_store_3d(&tmC, cstage + c * 32 * Cfg::BM, mrow0, nt * Cfg::BN + c * 32, b);
-                    ptx::bulk_commit_group();
+                        for (int j = 0; j < HALF; ++j) dst[j * Cfg::BM + r] = fmaf(p.alpha, creg[j], 0.0f);
+                        ptx::fence_proxy_async_smem();
+                    }
+                    ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                    if (leader) {
+#pragma unroll
+                        for (int c = 0; c < PART / 32; ++c)
+                            ptx::tma_store_3d(&tmC, cstage + c * 32 * Cfg::BM, mrow0, nt * Cfg::BN + part * PART + c * 32, b);
+                        ptx::bulk_commit_group();
+                    }
                 }
             } else {
                 const int r = mrow0 + (int)(q * 32 + lane);

@@ -497,10 +497,13 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     ptx::tmem_ld8(taddr + c * 8, vh);
                     ptx::tmem_ld8(taddr + BN + c * 8, vc);
                     ptx::tmem_wait_ld();
+                    if (p.corr) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float tt = p.corr ? fmaf(vc[j], scale, vh[j]) : vh[j];
-                        creg[c * 8 + j] = __fadd_rn(creg[c * 8 + j], tt);
+                        for (int j = 0; j < 8; j += 2)
+                            combine2(creg[c * 8 + j], creg[c * 8 + j + 1], vh[j], vh[j + 1], vc[j], vc[j + 1], scale);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) creg[c * 8 + j] = __fadd_rn(creg[c * 8 + j], vh[j]);
                     }
                 }
                 ptx::tc_fence_before();

@@ -59,6 +59,23 @@ __device__ __forceinline__ void split_fp16x2(float x0, float x1, uint32_t& hi, u
     lo = f32x2_to_f16x2_rn(r0, r1);
 }
 
+// combine step on two accumulator columns at once (R#8):
+//   t = RN(d_corr * scale + d_hi)  (one rounding: the FMA of Eq. corr-5's sum)
+//   c = RN(c + t)
+// on the packed FP32x2 pipe (FFMA2, FADD2), lane-wise identical to fmaf / __fadd_rn
+__device__ __forceinline__ void combine2(float& c0, float& c1, float hi0, float hi1, float co0, float co1, float scale)
+{
+    asm("{\n\t.reg .b64 h, k, s, t, c;\n\t"
+        "mov.b64 h, {%2, %3};\n\t"
+        "mov.b64 k, {%4, %5};\n\t"
+        "mov.b64 s, {%6, %6};\n\t"
+        "fma.rn.f32x2 t, k, s, h;\n\t"
+        "mov.b64 c, {%0, %1};\n\t"
+        "add.rn.f32x2 c, c, t;\n\t"
+        "mov.b64 {%0, %1}, c;\n\t}"
+        : "+f"(c0), "+f"(c1) : "f"(hi0), "f"(hi1), "f"(co0), "f"(co1), "f"(scale));
+}
+
 // four elements: (x0, x1) -> h01/l01, (x2, x3) -> h23/l23
 __device__ __forceinline__ void split_fp16x2x2(float x0, float x1, float x2, float x3, uint32_t& h01,
                                                uint32_t& h23, uint32_t& l01, uint32_t& l23)
