@@ -154,6 +154,16 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, long long count, 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// L2 prefetch distance (k-stages) of the TMA producer; EMU_PREFETCH overrides (tuning only)
+int prefetch_distance()
+{
+    static const int pf = [] {
+        const char* e = getenv("EMU_PREFETCH");
+        return e ? std::max(0, std::min(64, atoi(e))) : 0;   // measured: prefetch slows c2 (PF 8: -6 %)
+    }();
+    return pf;
+}
+
 emu_status launch_status(cudaError_t e)
 {
     if (e == cudaSuccess) return EMU_STATUS_SUCCESS;
@@ -209,6 +219,7 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     p.tma_store = tma_store;
+    p.prefetch = prefetch_distance();
     p.A = A; p.B = B; p.lda = lda; p.ldb = ldb;
     p.strideA = a_b ? strideA : 0; p.strideB = b_b ? strideB : 0;
 
@@ -271,6 +282,7 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     p.kb_stages = (kblock > 0 ? kblock : 64) / Cfg::BK;
     p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
     p.tma_store = tma_store;
+    p.prefetch = prefetch_distance();
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
     emu::emu_sgemm_pair_kernel<MODE, ALAY, RANGE>

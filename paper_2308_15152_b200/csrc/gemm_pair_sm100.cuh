@@ -63,9 +63,15 @@ struct PairCfg {
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
     static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + CSTAGE_BYTES + BAR_BYTES;
-    static constexpr int SPLIT_WARP0 = 2, NUM_SPLIT_WARPS = 8;
-    static constexpr int EPI_WARP0 = 10, NUM_EPI_WARPS = 8;
+    // warpgroup 0: TMA producer (warp 0), MMA issuer + TMEM owner (warp 1), 2 idle;
+    // warpgroups 1-4: 16 splitter warps; warpgroups 5-6: 8 combine/epilogue warps.
+    // Registers are re-balanced per warpgroup with setmaxnreg (launch: 72/thread).
+    static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 16;
+    static constexpr int EPI_WARP0 = 20, NUM_EPI_WARPS = 8;
     static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
+    static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = 56, REGS_EPI = 120;
+    static_assert(128 * REGS_CTRL + 32 * NUM_SPLIT_WARPS * REGS_SPLIT + 32 * NUM_EPI_WARPS * REGS_EPI <= 65536,
+                  "register budget");
     static_assert(SMEM_BYTES <= 232448, "shared memory");
     static_assert(ALAY != A_MN_SW128 || ESZ == 2, "MN-major SW128 here is the 16-bit layout");
 };
@@ -131,10 +137,12 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
     const int nks = p.num_k_stages;
     const int nkb = (nks + p.kb_stages - 1) / p.kb_stages;
 
-    if (warp == 0) {
+    if (warp < 4) {
+      ptx::setmaxnreg_dec<Cfg::REGS_CTRL>();
+      if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
         if (ptx::elect_one()) {
-            constexpr int PF = 8;
+            const int PF = p.prefetch;
             long long pt = cid;
             int pks = 0;
             auto prefetch_next = [&]() {
@@ -146,6 +154,7 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                 if (++pks == nks) { pks = 0; pt += ncl; }
             };
             for (int i = 0; i < PF; ++i) prefetch_next();
+            const bool do_pf = PF > 0;
             uint32_t s = 0, ph = 0;
             for (long long t = cid; t < p.num_tiles; t += ncl) {
                 int b, mt, nt;
@@ -160,12 +169,12 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                     ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab);
                     ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
                                             nt * Cfg::BN + rank * Cfg::BNC, bb);
-                    prefetch_next();
+                    if (do_pf) prefetch_next();
                     if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                 }
             }
         }
-    } else if (warp == 1) {
+      } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader CTA only)
         if (rank == 0 && ptx::elect_one()) {
             constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, Cfg::A_MAJOR, 0u, 256, Cfg::BN);
@@ -222,12 +231,14 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                 }
             }
         }
+      }
     } else if (warp >= Cfg::SPLIT_WARP0 && warp < Cfg::SPLIT_WARP0 + Cfg::NUM_SPLIT_WARPS) {
-        // ------------------------------------------------ splitters (256 threads)
-        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;   // 0..255
-        const uint32_t sw = tid >> 5;
-        const uint32_t row = tid & 127, half = tid >> 7;             // A K-major rows (TF32)
-        const uint32_t n = tid & 63, quarter = tid >> 6;             // B rows: 8 k per thread
+        // ------------------------------------------------ splitters (512 threads)
+        ptx::setmaxnreg_dec<Cfg::REGS_SPLIT>();
+        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;   // 0..511
+        const uint32_t sw = tid >> 5;                                 // 0..15
+        const uint32_t row = tid & 127, quarter = tid >> 7;          // A K-major (TF32): 8 k per thread
+        const uint32_t n = tid & 63, eighth = tid >> 6;              // B: 4 k per thread
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
         uint32_t nonfinite = 0;
         for (long long t = cid; t < p.num_tiles; t += ncl) {
@@ -247,28 +258,25 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                 uint8_t* ob_hi = o + 2 * Cfg::AOP_BYTES;
                 uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
                 // ---- load phase (all loads of the stage before the first store)
-                float4 va[4], vb[2];
+                float4 va[2], vb;
                 if (ALAY == A_K_SW128) {
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const float* col = reinterpret_cast<const float*>(fa) + 4 * (half * 4 + jj) * Cfg::BM + row;
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const float* col = reinterpret_cast<const float*>(fa) + 4 * (quarter * 2 + jj) * Cfg::BM + row;
                         va[jj] = make_float4(col[0], col[Cfg::BM], col[2 * Cfg::BM], col[3 * Cfg::BM]);
                     }
                 } else {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        va[kk] = *reinterpret_cast<const float4*>(fa + (sw + 8 * kk) * 512 + lane * 16);
+                    for (int kk = 0; kk < 2; ++kk)
+                        va[kk] = *reinterpret_cast<const float4*>(fa + (sw + 16 * kk) * 512 + lane * 16);
                 }
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {   // B(k = 8 quarter + 4c .. +3, n): 16-byte chunk 2 quarter + c
-                    const uint32_t ch = 2 * quarter + c;
-                    vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + ((ch ^ (n & 7)) << 4));
-                }
+                // B(k = 4 eighth .. +3, n): FP32 16-byte chunk `eighth` of row n
+                vb = *reinterpret_cast<const float4*>(fb + n * 128 + ((eighth ^ (n & 7)) << 4));
                 // ---- split + store phase
                 if (ALAY == A_K_SW128) {
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const uint32_t j = half * 4 + jj;
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const uint32_t j = quarter * 2 + jj;
                         uint4 hv, lv;
                         split_tf32(va[jj].x, hv.x, lv.x);
                         split_tf32(va[jj].y, hv.y, lv.y);
@@ -280,8 +288,8 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                     }
                 } else {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t k = sw + 8 * kk;
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const uint32_t k = sw + 16 * kk;
                         const uint32_t g = k >> 3, kr = k & 7;
                         uint2 h, l;
                         split4_fp16(va[kk], h, l);
@@ -294,29 +302,24 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                     }
                 }
                 if (MODE == 0) {
-                    // one 16-byte FP16 chunk (8 k) per thread, K-major SWIZZLE_64B rows
-                    uint2 h0, l0, h1, l1;
-                    split4_fp16(vb[0], h0, l0);
-                    split4_fp16(vb[1], h1, l1);
-                    if (RANGE)
-                        nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) | f16x2_nonfinite(h1.x) |
-                                     f16x2_nonfinite(h1.y);
-                    const uint32_t off = n * 64 + ((quarter ^ ((n >> 1) & 3)) << 4);
-                    *reinterpret_cast<uint4*>(ob_hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
-                    *reinterpret_cast<uint4*>(ob_lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+                    // half of a 16-byte FP16 chunk (4 k), K-major SWIZZLE_64B rows
+                    uint2 h, l;
+                    split4_fp16(vb, h, l);
+                    if (RANGE) nonfinite |= f16x2_nonfinite(h.x) | f16x2_nonfinite(h.y);
+                    const uint32_t j = eighth >> 1;
+                    const uint32_t off = n * 64 + ((j ^ ((n >> 1) & 3)) << 4) + (eighth & 1) * 8;
+                    *reinterpret_cast<uint2*>(ob_hi + off) = h;
+                    *reinterpret_cast<uint2*>(ob_lo + off) = l;
                 } else {
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {   // two 16-byte TF32 chunks, K-major SWIZZLE_128B rows
-                        const uint32_t j = 2 * quarter + c;
-                        uint4 h, l;
-                        split_tf32(vb[c].x, h.x, l.x);
-                        split_tf32(vb[c].y, h.y, l.y);
-                        split_tf32(vb[c].z, h.z, l.z);
-                        split_tf32(vb[c].w, h.w, l.w);
-                        const uint32_t off = n * 128 + ((j ^ (n & 7)) << 4);
-                        *reinterpret_cast<uint4*>(ob_hi + off) = h;
-                        *reinterpret_cast<uint4*>(ob_lo + off) = l;
-                    }
+                    // one 16-byte TF32 chunk (4 k), K-major SWIZZLE_128B rows
+                    uint4 h, l;
+                    split_tf32(vb.x, h.x, l.x);
+                    split_tf32(vb.y, h.y, l.y);
+                    split_tf32(vb.z, h.z, l.z);
+                    split_tf32(vb.w, h.w, l.w);
+                    const uint32_t off = n * 128 + ((eighth ^ (n & 7)) << 4);
+                    *reinterpret_cast<uint4*>(ob_hi + off) = h;
+                    *reinterpret_cast<uint4*>(ob_lo + off) = l;
                 }
                 ptx::fence_proxy_async_smem();        // our st.shared -> visible to UMMA
                 __syncwarp();
@@ -335,6 +338,7 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
         }
     } else if (warp >= Cfg::EPI_WARP0) {
         // ------------------------------------------------ combine + epilogue (both CTAs)
+        ptx::setmaxnreg_inc<Cfg::REGS_EPI>();
         constexpr int HALF = Cfg::BN / 2;
         const uint32_t e = warp - Cfg::EPI_WARP0;
         const uint32_t q = warp & 3;
@@ -357,18 +361,18 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                 ptx::tc_fence_after();
                 const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * Cfg::BN + h * HALF;
 #pragma unroll
-                for (int c = 0; c < HALF / 8; ++c) {
-                    float vh[8], vc[8];
-                    ptx::tmem_ld8(taddr + c * 8, vh);
-                    ptx::tmem_ld8(taddr + Cfg::BN + c * 8, vc);
+                for (int c = 0; c < HALF / 16; ++c) {
+                    float vh[16], vc[16];
+                    ptx::tmem_ld16(taddr + c * 16, vh);
+                    ptx::tmem_ld16(taddr + Cfg::BN + c * 16, vc);
                     ptx::tmem_wait_ld();
                     if (p.corr) {
 #pragma unroll
-                        for (int j = 0; j < 8; j += 2)
-                            combine2(creg[c * 8 + j], creg[c * 8 + j + 1], vh[j], vh[j + 1], vc[j], vc[j + 1], scale);
+                        for (int j = 0; j < 16; j += 2)
+                            combine2(creg[c * 16 + j], creg[c * 16 + j + 1], vh[j], vh[j + 1], vc[j], vc[j + 1], scale);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) creg[c * 8 + j] = __fadd_rn(creg[c * 8 + j], vh[j]);
+                        for (int j = 0; j < 16; ++j) creg[c * 16 + j] = __fadd_rn(creg[c * 16 + j], vh[j]);
                     }
                 }
                 ptx::tc_fence_before();

@@ -78,6 +78,7 @@ struct GemmParams {
     int kb_stages;                // KB / 32
     int corr;                     // 1 = the paper's method; 0 = "correction off" control
     int tma_store;                // 1: epilogue stages C in shared memory and TMA-stores it (beta == 0)
+    int prefetch;                 // L2 prefetch distance in k-stages (0 = off)
     unsigned int* range_flag;     // nullable (FP16 mode only)
     // direct-load (LDG) variant only: operands read by the splitter warps
     const float* A;
@@ -223,7 +224,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (!LDG && ptx::elect_one()) {
             // L2 prefetch cursor PF stages ahead of the loads: deepens the memory
             // pipeline beyond the S32 shared-memory stages (the loads then hit L2)
-            constexpr int PF = 8;
+            const int PF = p.prefetch;
             long long pt = blockIdx.x;
             int pks = 0;
             auto prefetch_next = [&]() {
@@ -235,6 +236,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 if (++pks == nks) { pks = 0; pt += gridDim.x; }
             };
             for (int i = 0; i < PF; ++i) prefetch_next();
+            const bool do_pf = PF > 0;
             uint32_t s = 0, ph = 0;
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
                 int b, mt, nt;
@@ -248,7 +250,7 @@ emu_sgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
                     ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * Cfg::BM, ks * Cfg::BK, ab);
                     ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK, nt * BN, bb);
-                    prefetch_next();
+                    if (do_pf) prefetch_next();
                     if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                 }
             }

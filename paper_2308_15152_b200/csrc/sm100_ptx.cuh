@@ -154,6 +154,13 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last()
     return p;
 }
 
+// ------------------------------------------------------- register budgets
+// per-warpgroup register re-allocation (all 4 warps of a warpgroup execute it)
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs)); }
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs)); }
+
 // ---------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank()
 {
