@@ -12,6 +12,7 @@
 
 #include "emu_sgemm.h"
 #include "gemm_pair_sm100.cuh"
+#include "gemm_pair_ts_sm100.cuh"
 #include "gemm_sm100.cuh"
 #include "split.cuh"
 
@@ -44,6 +45,7 @@ struct DeviceInfo {
     int sms = 0;
     bool attr_set[32] = {};
     bool pair_attr_set[16] = {};
+    bool ts_attr_set[4] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -291,6 +293,68 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
+template <int MODE, bool RANGE>
+emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
+                         long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
+                         long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
+                         unsigned flags)
+{
+    using Cfg = emu::PairTsCfg<MODE>;
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        const int slot = MODE * 2 + (RANGE ? 1 : 0);
+        if (!g_dev[dev].ts_attr_set[slot]) {
+            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
+                return EMU_STATUS_CUDA_ERROR;
+            g_dev[dev].ts_attr_set[slot] = true;
+        }
+    }
+    const bool a_b = batch > 1 && strideA != 0;
+    const bool b_b = batch > 1 && strideB != 0;
+    const bool c_b = batch > 1;
+    CUtensorMap tmA, tmB, tmC;
+    std::memset(&tmA, 0, sizeof(tmA));
+    std::memset(&tmB, 0, sizeof(tmB));
+    std::memset(&tmC, 0, sizeof(tmC));
+    const uint64_t sA = a_b ? (uint64_t)strideA : (((uint64_t)lda * (uint64_t)k + 3) & ~uint64_t(3));
+    const uint64_t sB = b_b ? (uint64_t)strideB : (((uint64_t)ldb * (uint64_t)n + 3) & ~uint64_t(3));
+    if (!make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA, Cfg::BM, Cfg::BK,
+                  CU_TENSOR_MAP_SWIZZLE_NONE))
+        return EMU_STATUS_NOT_SUPPORTED;
+    if (!make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB, Cfg::BK, Cfg::BNC,
+                  CU_TENSOR_MAP_SWIZZLE_128B))
+        return EMU_STATUS_NOT_SUPPORTED;
+    int tma_store = beta == 0.0f && aligned16(C) && ldc % 4 == 0 && (!c_b || strideC % 4 == 0) &&
+                    (unsigned long long)strideC * 4 < (1ull << 40);
+    if (tma_store) {
+        const uint64_t sC = c_b ? (uint64_t)strideC : (((uint64_t)ldc * (uint64_t)n + 3) & ~uint64_t(3));
+        if (!make_map(&tmC, C, (uint64_t)m, (uint64_t)n, (uint64_t)ldc, c_b ? (uint64_t)batch : 1, sC, Cfg::BM, 32,
+                      CU_TENSOR_MAP_SWIZZLE_NONE))
+            tma_store = 0;
+    }
+    emu::GemmParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.m = m; p.n = n; p.k = k;
+    p.a_batched = a_b; p.b_batched = b_b;
+    p.alpha = alpha; p.beta = beta;
+    p.C = C; p.ldc = ldc; p.strideC = strideC;
+    p.tiles_m = (m + 255) / 256;
+    p.tiles_n = (n + Cfg::BN - 1) / Cfg::BN;
+    p.num_tiles = (long long)p.tiles_m * p.tiles_n * batch;
+    p.num_k_stages = (k + Cfg::BK - 1) / Cfg::BK;
+    p.kb_stages = (kblock > 0 ? kblock : 64) / Cfg::BK;
+    p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
+    p.tma_store = tma_store;
+    p.prefetch = prefetch_distance();
+    p.range_flag = MODE == 0 ? range_flag : nullptr;
+    const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
+    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE>
+        <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+    g_last_launches = 1;
+    return launch_status(cudaGetLastError());
+}
+
 }  // namespace
 
 extern "C" {
@@ -355,12 +419,29 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     const bool ldg = !tma_ok || force_ldg;
     // CTA-pair kernel for problems with more than one 128-row block
     static const int kernel_pref = [] {
-        const char* e = getenv("EMU_KERNEL");   // "single" | "pair": tuning/diagnostics only
+        const char* e = getenv("EMU_KERNEL");   // "single" | "pair" | "ts": tuning/diagnostics only
         if (e && strcmp(e, "single") == 0) return 1;
         if (e && strcmp(e, "pair") == 0) return 2;
+        if (e && strcmp(e, "ts") == 0) return 3;
         return 0;
     }();
-    const bool pair = !ldg && (kernel_pref == 2 || (kernel_pref == 0 && m > 128));
+    // A-in-TMEM pair kernel: fewest shared-memory bytes per MMA but a single TMEM
+    // accumulator buffer (the MMA waits for each k-block's drain) -- it wins while
+    // the problem is memory-bound (short k per tile), the SMEM-operand pair kernel
+    // (double-buffered accumulators) wins for long k (profiles/r01_summary.md)
+    const bool ts = !ldg && (kernel_pref == 3 || (kernel_pref == 0 && m > 128 && k <= 512));
+    const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
+#define EMU_RUN_TS(MODE_, RANGE_)                                                                                  \
+    return run_gemm_pair_ts<MODE_, RANGE_>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, \
+                                           strideC, batch, s, d_range_flag, kblock, flags)
+    if (ts) {
+        if (mode == EMU_SPLIT_FP16) {
+            if (d_range_flag) EMU_RUN_TS(0, true);
+            EMU_RUN_TS(0, false);
+        }
+        EMU_RUN_TS(1, false);
+    }
+#undef EMU_RUN_TS
 #define EMU_RUN_PAIR(MODE_, ALAY_, RANGE_)                                                                          \
     return run_gemm_pair<MODE_, ALAY_, RANGE_>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, \
                                                ldc, strideC, batch, s, d_range_flag, kblock, flags)

@@ -429,9 +429,9 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
         if (p.tma_store && warp == Cfg::EPI_WARP0 && lane == 0) ptx::bulk_wait_group0();
     }
 #ifdef EMU_PROF
-    if (warp >= 2 || lane == 0) {
-        prof_acc[P_CTA_TOTAL] = (warp == 2 && lane == 0) ? (unsigned long long)(clock64() - prof_start) : 0;
-        PROF_FLUSH();
+    if (warp == 0 || warp == 1 || warp >= 4 || lane == 0) {
+        prof_acc[P_CTA_TOTAL] = (warp == 4 && lane == 0) ? (unsigned long long)(clock64() - prof_start) : 0;
+        if (warp != 2 && warp != 3) PROF_FLUSH();
     }
 #endif
 

@@ -1,0 +1,384 @@
+// gemm_pair_ts_sm100.cuh -- CTA-pair kernel with the A operand in TENSOR memory.
+//
+// The paper's point is that the split operands should not
+// make an extra round trip through shared memory.  On B200 the tensor core can
+// take A from TMEM: here the splitter warps write A_hi / A_lo with tcgen05.st
+// straight into TMEM (each warp its own 32-lane quadrant, lane = row m, K along
+// 32-bit columns, two FP16 values per column), so per 32-k stage and CTA the
+// shared-memory traffic drops from 108 KB (A and B both staged and read by the
+// MMA) to 68 KB (TMA writes and splitter reads of the FP32 tiles, B_hi/B_lo
+// writes, tensor-core reads of B only).
+//
+// Tile (per cluster of two CTAs): 256 (m) x 128 (n); MMA cta_group::2, M = 256,
+// N = 128 per instruction (tools/probe_mma: N = 64 instructions run at 47-68 %
+// of the N = 128 rate, so the accumulator is NOT split into column halves).
+// TMEM per CTA: D_hi [0,128), D_corr [128,256), then SOP A stages.  With A in
+// TMEM there is no room for a second accumulator buffer: the MMA of k-block j+1
+// waits until the combine warps have drained k-block j.
+// CTA r stages A rows [256 mt + 128 r, +128) and B columns [128 nt + 64 r, +64).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+
+#include "gemm_sm100.cuh"
+#include "sm100_ptx.cuh"
+#include "split.cuh"
+
+namespace emu {
+
+template <int MODE>
+struct PairTsCfg {
+    static constexpr int BM = 128;                      // A rows per CTA (pair M = 256)
+    static constexpr int BN = 128;                      // pair tile N = D columns per CTA
+    static constexpr int NH = 128;                      // MMA N
+    static constexpr int BNC = 64;                      // B columns staged per CTA
+    static constexpr int BK = 32;
+    static constexpr int ESZ = MODE == 0 ? 2 : 4;
+    static constexpr int KSTEP = MODE == 0 ? 16 : 8;
+    static constexpr int NSTEPS = BK / KSTEP;
+    static constexpr uint32_t A32_BYTES = BK * BM * 4;     // 16 KB
+    static constexpr uint32_t B32_BYTES = BK * BNC * 4;    //  8 KB
+    static constexpr uint32_t F32_STAGE = A32_BYTES + B32_BYTES;
+    static constexpr uint32_t BOP_BYTES = BNC * BK * ESZ;  // one of B_hi / B_lo
+    static constexpr uint32_t OP_STAGE = 2 * BOP_BYTES;
+    static constexpr int S32 = MODE == 0 ? 5 : 4;
+    static constexpr int SOP = 4;
+    static constexpr uint32_t CSTAGE_BYTES = BM * BN * 4;  // 64 KB TMA-store staging
+    static constexpr uint32_t B_ROW = BK * ESZ;            // 64 (FP16) / 128 (TF32) bytes
+    static constexpr uint32_t B_SBO = 8 * B_ROW;
+    static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;
+    // TMEM columns: D_hi [0,128), D_corr [128,256); A stages from column 256:
+    // per slot A_hi (ACOLS/2 columns) then A_lo
+    static constexpr uint32_t ACOLS = MODE == 0 ? 32 : 64;     // 32 k of hi + lo
+    static constexpr uint32_t A_COL0 = 256;
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t KCOLS = MODE == 0 ? 8 : 8;       // TMEM columns per MMA K step
+    static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
+    static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
+    static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + CSTAGE_BYTES + BAR_BYTES;
+    static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 16;
+    static constexpr int EPI_WARP0 = 20, NUM_EPI_WARPS = 8;
+    static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
+    static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = 56, REGS_EPI = 120;
+    static_assert(128 * REGS_CTRL + 32 * NUM_SPLIT_WARPS * REGS_SPLIT + 32 * NUM_EPI_WARPS * REGS_EPI <= 65536,
+                  "register budget");
+    static_assert(SMEM_BYTES <= 232448, "shared memory");
+};
+
+template <int MODE, bool RANGE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE>::NUM_THREADS, 1)
+emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, const GemmParams p)
+{
+    using Cfg = PairTsCfg<MODE>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* f32buf = smem;
+    uint8_t* opbuf = smem + Cfg::S32 * Cfg::F32_STAGE;
+    float* cstage = reinterpret_cast<float*>(opbuf + Cfg::SOP * Cfg::OP_STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(opbuf + Cfg::SOP * Cfg::OP_STAGE + Cfg::CSTAGE_BYTES);
+    uint64_t* f32_full = bars;
+    uint64_t* f32_empty = f32_full + Cfg::S32;
+    uint64_t* op_full = f32_empty + Cfg::S32;
+    uint64_t* op_empty = op_full + Cfg::SOP;
+    uint64_t* acc_full = op_empty + Cfg::SOP;   // [1] (second slot unused)
+    uint64_t* acc_empty = acc_full + 2;         // [1]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const uint32_t warp = ptx::warp_id();
+    const uint32_t lane = ptx::lane_id();
+    const uint32_t rank = ptx::cluster_ctarank();
+    const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    PROF_DECL
+#ifdef EMU_PROF
+    const long long prof_start = clock64();
+#endif
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < Cfg::S32; ++i) {
+            ptx::mbar_init(&f32_full[i], 1);
+            ptx::mbar_init(&f32_empty[i], Cfg::NUM_SPLIT_WARPS);
+        }
+        for (int i = 0; i < Cfg::SOP; ++i) {
+            ptx::mbar_init(&op_full[i], 2 * Cfg::NUM_SPLIT_WARPS);
+            ptx::mbar_init(&op_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&acc_full[i], 1);
+            ptx::mbar_init(&acc_empty[i], 2 * Cfg::NUM_EPI_WARPS);
+        }
+        ptx::fence_mbar_init();
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+    }
+    if (warp == 1) ptx::tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int nks = p.num_k_stages;
+    const int nkb = (nks + p.kb_stages - 1) / p.kb_stages;
+
+    if (warp < 4) {
+        ptx::setmaxnreg_dec<Cfg::REGS_CTRL>();
+        if (warp == 0) {
+            // -------------------------------------------- TMA producer (both CTAs)
+            if (ptx::elect_one()) {
+                uint32_t s = 0, ph = 0;
+                for (long long t = cid; t < p.num_tiles; t += ncl) {
+                    int b, mt, nt;
+                    tile_coords(p, t, b, mt, nt);
+                    const int ab = p.a_batched ? b : 0, bb = p.b_batched ? b : 0;
+                    for (int ks = 0; ks < nks; ++ks) {
+                        PROF_T0();
+                        ptx::mbar_wait_sleep(&f32_empty[s], ph ^ 1);
+                        PROF_ADD(P_PROD_WAIT_EMPTY);
+                        uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
+                        ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
+                        ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab);
+                        ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
+                                                nt * Cfg::BN + rank * Cfg::BNC, bb);
+                        if (++s == Cfg::S32) { s = 0; ph ^= 1; }
+                    }
+                }
+            }
+        } else if (warp == 1) {
+            // -------------------------------------------- MMA issuer (leader CTA only)
+            if (rank == 0 && ptx::elect_one()) {
+                constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 0u, 0u, 256, Cfg::NH);
+                uint32_t s = 0, ph = 0, acc_it = 0;
+                const uint32_t d_hi = tmem_base, d_corr = tmem_base + 128;
+                for (long long t = cid; t < p.num_tiles; t += ncl) {
+                    for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                        const int ks0 = kb * p.kb_stages;
+                        const int ks1 = min(ks0 + p.kb_stages, nks);
+                        PROF_T0();
+                        ptx::mbar_wait(&acc_empty[0], (acc_it & 1u) ^ 1u);
+                        PROF_ADD(P_MMA_WAIT_ACC);
+                        ptx::tc_fence_after();
+                        for (int ks = ks0; ks < ks1; ++ks) {
+                            PROF_T0();
+                            ptx::mbar_wait(&op_full[s], ph);
+                            PROF_ADD(P_MMA_WAIT_OP);
+                            PROF_T0();
+                            ptx::tc_fence_after();
+                            const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
+                            const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                            const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                            for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
+                                                                      Cfg::B_SBO, Cfg::B_LAYOUT);
+                                const uint32_t ka = st * Cfg::KCOLS;
+                                const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                if (MODE == 0) {
+                                    ptx::mma_f16_pair_ts(d_hi, a_hi + ka, dB_hi, idesc, acc);        // P1
+                                    if (p.corr) {
+                                        ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);  // P2
+                                        ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);   // P3
+                                    }
+                                } else {
+                                    ptx::mma_tf32_pair_ts(d_hi, a_hi + ka, dB_hi, idesc, acc);
+                                    if (p.corr) {
+                                        ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
+                                        ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
+                                    }
+                                }
+                            }
+                            ptx::tc_commit_pair(&op_empty[s], 0x3);   // slot free (both CTAs)
+                            PROF_ADD(P_MMA_ISSUE);
+                            if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                        }
+                        ptx::tc_commit_pair(&acc_full[0], 0x3);
+                    }
+                }
+            }
+        }
+    } else if (warp < Cfg::EPI_WARP0) {
+        // ------------------------------------------------ splitters (512 threads)
+        ptx::setmaxnreg_dec<Cfg::REGS_SPLIT>();
+        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;    // 0..511
+        const uint32_t q = warp & 3;                                  // TMEM lane quadrant
+        const uint32_t kq = (warp - Cfg::SPLIT_WARP0) >> 2;          // 8-k slice of the stage
+        const uint32_t m = q * 32 + lane;                             // A row (TMEM lane)
+        const uint32_t n = tid & 63, eighth = tid >> 6;               // B: 4 k per thread
+        const uint32_t tq = tmem_base + ((q * 32u) << 16);
+        uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
+        uint32_t nonfinite = 0;
+        for (long long t = cid; t < p.num_tiles; t += ncl) {
+            for (int ks = 0; ks < nks; ++ks) {
+                PROF_T0();
+                ptx::mbar_wait(&f32_full[s32], ph32);
+                PROF_ADD(P_SPL_WAIT_F32);
+                PROF_T0();
+                ptx::mbar_wait(&op_empty[sop], phop ^ 1);
+                PROF_ADD(P_SPL_WAIT_OP);
+                PROF_T0();
+                ptx::tc_fence_after();
+                const float* fa = reinterpret_cast<const float*>(f32buf + s32 * Cfg::F32_STAGE);
+                const uint8_t* fb = f32buf + s32 * Cfg::F32_STAGE + Cfg::A32_BYTES;
+                uint8_t* ob_hi = opbuf + sop * Cfg::OP_STAGE;
+                uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
+                // ---- load phase: A(m, 8 kq .. +7) (a warp reads 32 consecutive m per k) and B(4 eighth.., n)
+                float av[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) av[j] = fa[(kq * 8 + j) * Cfg::BM + m];
+                const float4 vb = *reinterpret_cast<const float4*>(fb + n * 128 + ((eighth ^ (n & 7)) << 4));
+                // ---- A: split into TMEM columns (lane = m)
+                const uint32_t a_hi = tq + Cfg::A_COL0 + sop * Cfg::ACOLS;
+                const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                if (MODE == 0) {
+                    uint32_t h[4], l[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) split_fp16x2(av[2 * j], av[2 * j + 1], h[j], l[j]);
+                    if (RANGE)
+                        nonfinite |= f16x2_nonfinite(h[0]) | f16x2_nonfinite(h[1]) | f16x2_nonfinite(h[2]) |
+                                     f16x2_nonfinite(h[3]);
+                    ptx::tmem_st4(a_hi + kq * 4, h[0], h[1], h[2], h[3]);
+                    ptx::tmem_st4(a_lo + kq * 4, l[0], l[1], l[2], l[3]);
+                } else {
+                    uint32_t h[8], l[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) split_tf32(av[j], h[j], l[j]);
+                    ptx::tmem_st8(a_hi + kq * 8, h);
+                    ptx::tmem_st8(a_lo + kq * 8, l);
+                }
+                // ---- B: split into the K-major operand tile in shared memory
+                if (MODE == 0) {
+                    uint2 h, l;
+                    split4_fp16(vb, h, l);
+                    if (RANGE) nonfinite |= f16x2_nonfinite(h.x) | f16x2_nonfinite(h.y);
+                    const uint32_t j = eighth >> 1;
+                    const uint32_t off = n * 64 + ((j ^ ((n >> 1) & 3)) << 4) + (eighth & 1) * 8;
+                    *reinterpret_cast<uint2*>(ob_hi + off) = h;
+                    *reinterpret_cast<uint2*>(ob_lo + off) = l;
+                } else {
+                    uint4 h, l;
+                    split_tf32(vb.x, h.x, l.x);
+                    split_tf32(vb.y, h.y, l.y);
+                    split_tf32(vb.z, h.z, l.z);
+                    split_tf32(vb.w, h.w, l.w);
+                    const uint32_t off = n * 128 + ((eighth ^ (n & 7)) << 4);
+                    *reinterpret_cast<uint4*>(ob_hi + off) = h;
+                    *reinterpret_cast<uint4*>(ob_lo + off) = l;
+                }
+                ptx::fence_proxy_async_smem();   // B tiles -> async proxy
+                ptx::tmem_wait_st();             // A columns written
+                ptx::tc_fence_before();
+                __syncwarp();
+                PROF_ADD(P_SPL_WORK);
+                if (lane == 0) {
+                    ptx::mbar_arrive_cluster(ptx::mapa_shared(&op_full[sop], 0));
+                    ptx::mbar_arrive(&f32_empty[s32]);
+                }
+                if (++s32 == Cfg::S32) { s32 = 0; ph32 ^= 1; }
+                if (++sop == Cfg::SOP) { sop = 0; phop ^= 1; }
+            }
+        }
+        if (RANGE) {
+            nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+            if (nonfinite && lane == 0) atomicOr(p.range_flag, 1u);
+        }
+    } else {
+        // ------------------------------------------------ combine + epilogue (both CTAs)
+        ptx::setmaxnreg_inc<Cfg::REGS_EPI>();
+        constexpr int HALF = Cfg::BN / 2;              // 64 columns: this warp's column half
+        const uint32_t e = warp - Cfg::EPI_WARP0;
+        const uint32_t q = warp & 3;
+        const uint32_t h = e >> 2;
+        const float scale = MODE == 0 ? (1.0f / 2048.0f) : 1.0f;
+        const uint32_t acc_empty_leader = ptx::mapa_shared(&acc_empty[0], 0);
+        uint32_t acc_it = 0;
+        for (long long t = cid; t < p.num_tiles; t += ncl) {
+            int b, mt, nt;
+            tile_coords(p, t, b, mt, nt);
+            float creg[HALF];
+#pragma unroll
+            for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
+            for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                PROF_T0();
+                ptx::mbar_wait_sleep(&acc_full[0], acc_it & 1u);
+                PROF_ADD(P_EPI_WAIT_ACC);
+                PROF_T0();
+                ptx::tc_fence_after();
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + h * HALF;
+#pragma unroll
+                for (int c = 0; c < HALF / 16; ++c) {
+                    float vh[16], vc[16];
+                    ptx::tmem_ld16(taddr + c * 16, vh);
+                    ptx::tmem_ld16(taddr + 128 + c * 16, vc);
+                    ptx::tmem_wait_ld();
+                    if (p.corr) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 2)
+                            combine2(creg[c * 16 + j], creg[c * 16 + j + 1], vh[j], vh[j + 1], vc[j], vc[j + 1], scale);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) creg[c * 16 + j] = __fadd_rn(creg[c * 16 + j], vh[j]);
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader);
+                PROF_ADD(P_EPI_DRAIN);
+            }
+            PROF_T0();
+            const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
+            if (p.tma_store) {
+                const bool leader = (e == 0 && lane == 0);
+                const uint32_t r = q * 32 + lane;
+                if (leader) ptx::bulk_wait_group_read0();
+                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                float* dst = cstage + h * HALF * Cfg::BM;
+#pragma unroll
+                for (int j = 0; j < HALF; ++j) dst[j * Cfg::BM + r] = fmaf(p.alpha, creg[j], 0.0f);
+                ptx::fence_proxy_async_smem();
+                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                if (leader) {
+#pragma unroll
+                    for (int c = 0; c < Cfg::BN / 32; ++c)
+                        ptx::tma_store_3d(&tmC, cstage + c * 32 * Cfg::BM, mrow0, nt * Cfg::BN + c * 32, b);
+                    ptx::bulk_commit_group();
+                }
+            } else {
+                const int r = mrow0 + (int)(q * 32 + lane);
+                const int col0 = nt * Cfg::BN + (int)(h * HALF);
+                if (r < p.m) {
+                    float* cp = p.C + (long long)b * p.strideC + r + (long long)col0 * p.ldc;
+                    if (p.beta != 0.0f) {
+#pragma unroll
+                        for (int j = 0; j < HALF; ++j)
+                            if (col0 + j < p.n) {
+                                float* d = cp + (long long)j * p.ldc;
+                                *d = fmaf(p.alpha, creg[j], __fmul_rn(p.beta, *d));
+                            }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < HALF; ++j)
+                            if (col0 + j < p.n) cp[(long long)j * p.ldc] = fmaf(p.alpha, creg[j], 0.0f);
+                    }
+                }
+            }
+            PROF_ADD(P_EPI_STORE);
+        }
+        if (p.tma_store && warp == Cfg::EPI_WARP0 && lane == 0) ptx::bulk_wait_group0();
+    }
+#ifdef EMU_PROF
+    if (warp == 0 || warp == 1 || warp >= 4 || lane == 0) {
+        prof_acc[P_CTA_TOTAL] = (warp == 4 && lane == 0) ? (unsigned long long)(clock64() - prof_start) : 0;
+        if (warp != 2 && warp != 3) PROF_FLUSH();
+    }
+#endif
+
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair<Cfg::TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace emu

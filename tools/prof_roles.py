@@ -65,8 +65,11 @@ def main():
     tot = v["cta_total"] / ctas
     print(f"{cfg} mode={mode} {ms:.3f} ms/launch, {2.0 * m * n * k * batch / ms / 1e9:.1f} TF; "
           f"cycles per CTA {tot:.0f}")
-    per = {"prod_wait_empty": 1, "mma_wait_acc": 1, "mma_wait_op": 1, "mma_issue": 1, "spl_wait_f32": 8,
-           "spl_wait_op": 8, "spl_work": 8, "epi_wait_acc": 8, "epi_drain": 8, "epi_store": 8}
+    nspl = 8 if os.environ.get("EMU_KERNEL") == "single" or m <= 128 else 16
+    ctas_mma = ctas if nspl == 8 else ctas // 2     # pair kernels: the MMA issuer lives in the leader CTA
+    per = {"prod_wait_empty": 1, "mma_wait_acc": ctas_mma / ctas, "mma_wait_op": ctas_mma / ctas,
+           "mma_issue": ctas_mma / ctas, "spl_wait_f32": nspl, "spl_wait_op": nspl, "spl_work": nspl,
+           "epi_wait_acc": 8, "epi_drain": 8, "epi_store": 8}
     for k_, nw in per.items():
         print(f"  {k_:16s} {v[k_] / ctas / nw / tot * 100:6.1f}% of CTA time (per warp)")
 
