@@ -39,6 +39,25 @@ PAPER_A100 = {"value": 54.2, "unit": "TFlop/s", "hw": "A100 40GB SXM4", "fp32_si
               "cite": "PAPER.md P:33, P:557"}
 
 
+def shard(rank: int, world: int, batch_per_rank: int):
+    """Weak scaling over the batch (R#21): rank r owns problems
+    [r * batch_per_rank, (r + 1) * batch_per_rank) of the global batch; inputs are
+    generated per problem from (seed, global index), so every rank sees exactly
+    the data the single-GPU run would have for those problems."""
+    return rank * batch_per_rank, (rank + 1) * batch_per_rank
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """max of a per-rank timing over all ranks (identity without a process group)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -235,7 +254,8 @@ def main():
     mode = args.mode
 
     # inputs: this rank's contiguous block of problems (weak scaling)
-    A_h, B_h = workloads.make_operands(batch, m, n, k, cfg.seed, item0=rank * batch)
+    item0, _ = shard(rank, world, batch)
+    A_h, B_h = workloads.make_operands(batch, m, n, k, cfg.seed, item0=item0)
     dA = torch.from_numpy(A_h).cuda()
     dB = torch.from_numpy(B_h).cuda()
     dC = torch.empty((batch, n, m), device="cuda")
@@ -265,11 +285,7 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     flops_step = 2.0 * m * n * k * batch * world
     value = flops_step * args.steps / (ms_max / 1e3) / 1e12
     ms_per_step = ms_max / args.steps
@@ -306,10 +322,8 @@ def main():
         for _ in range(args.e2e_steps):
             emu.emu_sgemm_batched_host(m, n, k, 1.0, pA, m, sA, pB, k, sB, 0.0, pC, m, sC, batch, mode, stream)
         torch.cuda.synchronize()
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": flops_step * args.e2e_steps / float(dt.item()) / 1e12, "unit": UNIT,
+        dt = max_over_ranks(time.perf_counter() - t0, device="cuda")
+        e2e = {"value": flops_step * args.e2e_steps / dt / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": int(pA.numel() * 4 + pB.numel() * 4),
                "d2h_bytes_per_step": int(pC.numel() * 4), "steps": args.e2e_steps,
                "api": "emu_sgemm_batched_host (pinned host buffers)"}
