@@ -157,6 +157,12 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, long long count, 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // L2 prefetch distance (k-stages) of the TMA producer; EMU_PREFETCH overrides (tuning only)
+int env_int(const char* name, int dflt, int lo, int hi)
+{
+    const char* e = getenv(name);
+    return e ? std::max(lo, std::min(hi, atoi(e))) : dflt;
+}
+
 int prefetch_distance()
 {
     static const int pf = [] {
@@ -222,6 +228,12 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     p.tma_store = tma_store;
     p.prefetch = prefetch_distance();
+    {
+        static const int gm = env_int("EMU_GROUP_M", 4, 1, 1 << 20);    // tuning only (measured c3: 4 > 8, 16, 32)
+        static const int pol = env_int("EMU_L2_POLICY", 0, 0, 3);      // tuning only
+        p.group_m = gm;
+        p.l2_policy = pol;
+    }
     p.A = A; p.B = B; p.lda = lda; p.ldb = ldb;
     p.strideA = a_b ? strideA : 0; p.strideB = b_b ? strideB : 0;
 
@@ -285,6 +297,12 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
     p.tma_store = tma_store;
     p.prefetch = prefetch_distance();
+    {
+        static const int gm = env_int("EMU_GROUP_M", 4, 1, 1 << 20);    // tuning only (measured c3: 4 > 8, 16, 32)
+        static const int pol = env_int("EMU_L2_POLICY", 0, 0, 3);      // tuning only
+        p.group_m = gm;
+        p.l2_policy = pol;
+    }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
     emu::emu_sgemm_pair_kernel<MODE, ALAY, RANGE>
@@ -347,6 +365,12 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
     p.tma_store = tma_store;
     p.prefetch = prefetch_distance();
+    {
+        static const int gm = env_int("EMU_GROUP_M", 4, 1, 1 << 20);    // tuning only (measured c3: 4 > 8, 16, 32)
+        static const int pol = env_int("EMU_L2_POLICY", 0, 0, 3);      // tuning only
+        p.group_m = gm;
+        p.l2_policy = pol;
+    }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
     emu::emu_sgemm_pair_ts_kernel<MODE, RANGE>

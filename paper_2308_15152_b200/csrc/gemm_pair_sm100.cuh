@@ -155,6 +155,7 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
             };
             for (int i = 0; i < PF; ++i) prefetch_next();
             const bool do_pf = PF > 0;
+            const uint64_t pol_keep = ptx::l2_policy_evict_last();
             uint32_t s = 0, ph = 0;
             for (long long t = cid; t < p.num_tiles; t += ncl) {
                 int b, mt, nt;
@@ -166,9 +167,16 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
                     PROF_ADD(P_PROD_WAIT_EMPTY);
                     uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                     ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
-                    ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab);
-                    ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
-                                            nt * Cfg::BN + rank * Cfg::BNC, bb);
+                    if (p.l2_policy & 2)
+                        ptx::tma_load_3d(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab, pol_keep);
+                    else
+                        ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab);
+                    if (p.l2_policy & 1)
+                        ptx::tma_load_3d(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
+                                         nt * Cfg::BN + rank * Cfg::BNC, bb, pol_keep);
+                    else
+                        ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
+                                                nt * Cfg::BN + rank * Cfg::BNC, bb);
                     if (do_pf) prefetch_next();
                     if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                 }

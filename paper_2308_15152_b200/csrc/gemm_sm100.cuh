@@ -79,6 +79,8 @@ struct GemmParams {
     int corr;                     // 1 = the paper's method; 0 = "correction off" control
     int tma_store;                // 1: epilogue stages C in shared memory and TMA-stores it (beta == 0)
     int prefetch;                 // L2 prefetch distance in k-stages (0 = off)
+    int group_m;                  // raster: m-tiles per group walking the n-tiles together
+    int l2_policy;                // 0 default; 1 B evict_last; 2 A evict_last; 3 both
     unsigned int* range_flag;     // nullable (FP16 mode only)
     // direct-load (LDG) variant only: operands read by the splitter warps
     const float* A;
@@ -136,14 +138,14 @@ struct GemmCfg {
     static_assert(BN == 128, "this kernel's splitter work division assumes BN = 128");
 };
 
-// tile index -> (batch, m-tile, n-tile); groups of up to 16 m-tiles walk the
+// tile index -> (batch, m-tile, n-tile); groups of up to group_m m-tiles walk the
 // n-tiles together so that concurrently running CTAs share A and B in L2.
 __device__ __forceinline__ void tile_coords(const GemmParams& p, long long t, int& b, int& mt, int& nt)
 {
     const long long per_batch = (long long)p.tiles_m * p.tiles_n;
     b = (int)(t / per_batch);
     int r = (int)(t - (long long)b * per_batch);
-    const int GM = p.tiles_m < 16 ? p.tiles_m : 16;
+    const int GM = p.tiles_m < p.group_m ? p.tiles_m : p.group_m;
     const int group = r / (GM * p.tiles_n);
     const int first_m = group * GM;
     const int gm = (p.tiles_m - first_m) < GM ? (p.tiles_m - first_m) : GM;
