@@ -450,10 +450,12 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
         return 0;
     }();
     // A-in-TMEM pair kernel: fewest shared-memory bytes per MMA but a single TMEM
-    // accumulator buffer (the MMA waits for each k-block's drain) -- it wins while
-    // the problem is memory-bound (short k per tile), the SMEM-operand pair kernel
-    // (double-buffered accumulators) wins for long k (profiles/r01_summary.md)
-    const bool ts = !ldg && (kernel_pref == 3 || (kernel_pref == 0 && m > 128 && k <= 512));
+    // accumulator buffer (the MMA waits for each k-block's drain).  Measured
+    // (profiles/r01_summary.md): it wins for FP16 at every size and for TF32 with
+    // short k; the SMEM-operand pair kernel (double-buffered accumulators) wins for
+    // TF32 with long k, whose MMAs are twice as long per operand byte.
+    const bool ts = !ldg && (kernel_pref == 3 ||
+                             (kernel_pref == 0 && m > 128 && (mode == EMU_SPLIT_FP16 || k <= 512)));
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
 #define EMU_RUN_TS(MODE_, RANGE_)                                                                                  \
     return run_gemm_pair_ts<MODE_, RANGE_>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, \

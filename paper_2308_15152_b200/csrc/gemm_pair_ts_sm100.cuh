@@ -57,10 +57,16 @@ struct PairTsCfg {
     static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
     static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
     static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + CSTAGE_BYTES + BAR_BYTES;
-    static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 16;
-    static constexpr int EPI_WARP0 = 20, NUM_EPI_WARPS = 8;
+    // warpgroup 0: producer, MMA issuer, 2 idle; warpgroups 1-2: 8 splitter warps
+    // (2 per TMEM lane quadrant, 16 k each); warpgroups 3-6: 16 combine warps (4 per
+    // lane quadrant, 32 accumulator columns each -- a short drain matters here
+    // because the single accumulator buffer makes the MMA wait for it)
+    static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 8;
+    static constexpr int EPI_WARP0 = 12, NUM_EPI_WARPS = 16;
     static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
-    static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = 56, REGS_EPI = 120;
+    static constexpr int KS = BK / (NUM_SPLIT_WARPS / 4);   // k per splitter warp (A)
+    static constexpr int ECOLS = BN / (NUM_EPI_WARPS / 4);  // accumulator columns per combine warp
+    static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = 64, REGS_EPI = 80;
     static_assert(128 * REGS_CTRL + 32 * NUM_SPLIT_WARPS * REGS_SPLIT + 32 * NUM_EPI_WARPS * REGS_EPI <= 65536,
                   "register budget");
     static_assert(SMEM_BYTES <= 232448, "shared memory");
@@ -198,13 +204,13 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             }
         }
     } else if (warp < Cfg::EPI_WARP0) {
-        // ------------------------------------------------ splitters (512 threads)
+        // ------------------------------------------------ splitters (256 threads)
         ptx::setmaxnreg_dec<Cfg::REGS_SPLIT>();
-        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;    // 0..511
+        const uint32_t tid = threadIdx.x - Cfg::SPLIT_WARP0 * 32;    // 0..255
         const uint32_t q = warp & 3;                                  // TMEM lane quadrant
-        const uint32_t kq = (warp - Cfg::SPLIT_WARP0) >> 2;          // 8-k slice of the stage
+        const uint32_t kq = (warp - Cfg::SPLIT_WARP0) >> 2;          // KS-k slice of the stage
         const uint32_t m = q * 32 + lane;                             // A row (TMEM lane)
-        const uint32_t n = tid & 63, eighth = tid >> 6;               // B: 4 k per thread
+        const uint32_t n = tid & 63, quarter = tid >> 6;              // B: 8 k per thread
         const uint32_t tq = tmem_base + ((q * 32u) << 16);
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
         uint32_t nonfinite = 0;
@@ -222,48 +228,62 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 const uint8_t* fb = f32buf + s32 * Cfg::F32_STAGE + Cfg::A32_BYTES;
                 uint8_t* ob_hi = opbuf + sop * Cfg::OP_STAGE;
                 uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
-                // ---- load phase: A(m, 8 kq .. +7) (a warp reads 32 consecutive m per k) and B(4 eighth.., n)
-                float av[8];
+                // ---- load phase: A(m, KS kq .. +KS-1) (a warp reads 32 consecutive m per k),
+                //      B(8 quarter .. +7, n): FP32 16-byte chunks 2 quarter, 2 quarter + 1 of row n
+                float av[Cfg::KS];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) av[j] = fa[(kq * 8 + j) * Cfg::BM + m];
-                const float4 vb = *reinterpret_cast<const float4*>(fb + n * 128 + ((eighth ^ (n & 7)) << 4));
+                for (int j = 0; j < Cfg::KS; ++j) av[j] = fa[(kq * Cfg::KS + j) * Cfg::BM + m];
+                float4 vb[2];
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
                 // ---- A: split into TMEM columns (lane = m)
                 const uint32_t a_hi = tq + Cfg::A_COL0 + sop * Cfg::ACOLS;
                 const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
                 if (MODE == 0) {
-                    uint32_t h[4], l[4];
+                    uint32_t h[Cfg::KS / 2], l[Cfg::KS / 2];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) split_fp16x2(av[2 * j], av[2 * j + 1], h[j], l[j]);
-                    if (RANGE)
-                        nonfinite |= f16x2_nonfinite(h[0]) | f16x2_nonfinite(h[1]) | f16x2_nonfinite(h[2]) |
-                                     f16x2_nonfinite(h[3]);
-                    ptx::tmem_st4(a_hi + kq * 4, h[0], h[1], h[2], h[3]);
-                    ptx::tmem_st4(a_lo + kq * 4, l[0], l[1], l[2], l[3]);
+                    for (int j = 0; j < Cfg::KS / 2; ++j) {
+                        split_fp16x2(av[2 * j], av[2 * j + 1], h[j], l[j]);
+                        if (RANGE) nonfinite |= f16x2_nonfinite(h[j]);
+                    }
+                    ptx::tmem_st8(a_hi + kq * (Cfg::KS / 2), h);
+                    ptx::tmem_st8(a_lo + kq * (Cfg::KS / 2), l);
                 } else {
-                    uint32_t h[8], l[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) split_tf32(av[j], h[j], l[j]);
-                    ptx::tmem_st8(a_hi + kq * 8, h);
-                    ptx::tmem_st8(a_lo + kq * 8, l);
+                    for (int c = 0; c < Cfg::KS / 8; ++c) {
+                        uint32_t h[8], l[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) split_tf32(av[8 * c + j], h[j], l[j]);
+                        ptx::tmem_st8(a_hi + kq * Cfg::KS + 8 * c, h);
+                        ptx::tmem_st8(a_lo + kq * Cfg::KS + 8 * c, l);
+                    }
                 }
                 // ---- B: split into the K-major operand tile in shared memory
                 if (MODE == 0) {
-                    uint2 h, l;
-                    split4_fp16(vb, h, l);
-                    if (RANGE) nonfinite |= f16x2_nonfinite(h.x) | f16x2_nonfinite(h.y);
-                    const uint32_t j = eighth >> 1;
-                    const uint32_t off = n * 64 + ((j ^ ((n >> 1) & 3)) << 4) + (eighth & 1) * 8;
-                    *reinterpret_cast<uint2*>(ob_hi + off) = h;
-                    *reinterpret_cast<uint2*>(ob_lo + off) = l;
+                    // one 16-byte FP16 chunk (8 k), K-major SWIZZLE_64B rows
+                    uint2 h0, l0, h1, l1;
+                    split4_fp16(vb[0], h0, l0);
+                    split4_fp16(vb[1], h1, l1);
+                    if (RANGE)
+                        nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) | f16x2_nonfinite(h1.x) |
+                                     f16x2_nonfinite(h1.y);
+                    const uint32_t off = n * 64 + ((quarter ^ ((n >> 1) & 3)) << 4);
+                    *reinterpret_cast<uint4*>(ob_hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+                    *reinterpret_cast<uint4*>(ob_lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
                 } else {
-                    uint4 h, l;
-                    split_tf32(vb.x, h.x, l.x);
-                    split_tf32(vb.y, h.y, l.y);
-                    split_tf32(vb.z, h.z, l.z);
-                    split_tf32(vb.w, h.w, l.w);
-                    const uint32_t off = n * 128 + ((eighth ^ (n & 7)) << 4);
-                    *reinterpret_cast<uint4*>(ob_hi + off) = h;
-                    *reinterpret_cast<uint4*>(ob_lo + off) = l;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {   // two 16-byte TF32 chunks, K-major SWIZZLE_128B rows
+                        const uint32_t j = 2 * quarter + c;
+                        uint4 h, l;
+                        split_tf32(vb[c].x, h.x, l.x);
+                        split_tf32(vb[c].y, h.y, l.y);
+                        split_tf32(vb[c].z, h.z, l.z);
+                        split_tf32(vb[c].w, h.w, l.w);
+                        const uint32_t off = n * 128 + ((j ^ (n & 7)) << 4);
+                        *reinterpret_cast<uint4*>(ob_hi + off) = h;
+                        *reinterpret_cast<uint4*>(ob_lo + off) = l;
+                    }
                 }
                 ptx::fence_proxy_async_smem();   // B tiles -> async proxy
                 ptx::tmem_wait_st();             // A columns written
@@ -285,10 +305,10 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     } else {
         // ------------------------------------------------ combine + epilogue (both CTAs)
         ptx::setmaxnreg_inc<Cfg::REGS_EPI>();
-        constexpr int HALF = Cfg::BN / 2;              // 64 columns: this warp's column half
+        constexpr int HALF = Cfg::ECOLS;               // this warp's accumulator columns
         const uint32_t e = warp - Cfg::EPI_WARP0;
         const uint32_t q = warp & 3;
-        const uint32_t h = e >> 2;
+        const uint32_t h = e >> 2;                     // column group
         const float scale = MODE == 0 ? (1.0f / 2048.0f) : 1.0f;
         const uint32_t acc_empty_leader = ptx::mapa_shared(&acc_empty[0], 0);
         uint32_t acc_it = 0;
