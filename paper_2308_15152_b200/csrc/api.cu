@@ -45,7 +45,7 @@ struct DeviceInfo {
     int sms = 0;
     bool attr_set[32] = {};
     bool pair_attr_set[16] = {};
-    bool ts_attr_set[4] = {};
+    bool ts_attr_set[8] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -311,18 +311,18 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
-template <int MODE, bool RANGE>
+template <int MODE, bool RANGE, int BN>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
                          unsigned flags)
 {
-    using Cfg = emu::PairTsCfg<MODE>;
+    using Cfg = emu::PairTsCfg<MODE, BN>;
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        const int slot = MODE * 2 + (RANGE ? 1 : 0);
+        const int slot = (MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1);
         if (!g_dev[dev].ts_attr_set[slot]) {
-            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE>,
+            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
                 return EMU_STATUS_CUDA_ERROR;
             g_dev[dev].ts_attr_set[slot] = true;
@@ -373,7 +373,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
-    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE>
+    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN>
         <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
@@ -449,17 +449,24 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
         if (e && strcmp(e, "ts") == 0) return 3;
         return 0;
     }();
-    // A-in-TMEM pair kernel: fewest shared-memory bytes per MMA but a single TMEM
-    // accumulator buffer (the MMA waits for each k-block's drain).  Measured
-    // (profiles/r01_summary.md): it wins for FP16 at every size and for TF32 with
-    // short k; the SMEM-operand pair kernel (double-buffered accumulators) wins for
-    // TF32 with long k, whose MMAs are twice as long per operand byte.
-    const bool ts = !ldg && (kernel_pref == 3 ||
-                             (kernel_pref == 0 && m > 128 && (mode == EMU_SPLIT_FP16 || k <= 512)));
+    // A-in-TMEM pair kernel (fewest shared-memory bytes per MMA) for every problem
+    // with more than one 128-row block; the SMEM-operand pair kernel stays selectable
+    // (EMU_KERNEL=pair) for comparison.
+    const bool ts = !ldg && (kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
-#define EMU_RUN_TS(MODE_, RANGE_)                                                                                  \
-    return run_gemm_pair_ts<MODE_, RANGE_>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, \
-                                           strideC, batch, s, d_range_flag, kblock, flags)
+    // tile width of the TS kernel (profiles/r01_summary.md): 128 (one accumulator
+    // buffer) for FP16 and short-k TF32; 96 (two buffers, the MMA never waits for a
+    // drain) for long-k TF32, whose MMAs are long enough to hide the extra A split.
+    static const int ts_n_env = env_int("EMU_TS_N", 0, 0, 128);   // tuning only
+    const int ts_n = ts_n_env ? ts_n_env : ((mode == EMU_SPLIT_FP16 || k <= 512) ? 128 : 96);
+#define EMU_RUN_TS(MODE_, RANGE_)                                                                                      \
+    do {                                                                                                               \
+        if (ts_n == 128)                                                                                               \
+            return run_gemm_pair_ts<MODE_, RANGE_, 128>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB,   \
+                                                        beta, C, ldc, strideC, batch, s, d_range_flag, kblock, flags); \
+        return run_gemm_pair_ts<MODE_, RANGE_, 96>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,  \
+                                                   C, ldc, strideC, batch, s, d_range_flag, kblock, flags);           \
+    } while (0)
     if (ts) {
         if (mode == EMU_SPLIT_FP16) {
             if (d_range_flag) EMU_RUN_TS(0, true);

@@ -9,13 +9,14 @@
 // MMA) to 68 KB (TMA writes and splitter reads of the FP32 tiles, B_hi/B_lo
 // writes, tensor-core reads of B only).
 //
-// Tile (per cluster of two CTAs): 256 (m) x 128 (n); MMA cta_group::2, M = 256,
-// N = 128 per instruction (tools/probe_mma: N = 64 instructions run at 47-68 %
-// of the N = 128 rate, so the accumulator is NOT split into column halves).
-// TMEM per CTA: D_hi [0,128), D_corr [128,256), then SOP A stages.  With A in
-// TMEM there is no room for a second accumulator buffer: the MMA of k-block j+1
-// waits until the combine warps have drained k-block j.
-// CTA r stages A rows [256 mt + 128 r, +128) and B columns [128 nt + 64 r, +64).
+// Tile (per cluster of two CTAs): 256 (m) x BN (n); MMA cta_group::2, M = 256,
+// N = BN per instruction (tools/probe_mma: A-from-TMEM MMAs run at the full
+// tensor rate for any N multiple of 16).  TMEM per CTA: DBUF accumulator buffers
+// of (D_hi, D_corr) x BN columns, then SOP A stages:
+//   BN =  96: 2 buffers (384 columns) + A -- the MMA of k-block j+1 overlaps the
+//             drain of k-block j (the default);
+//   BN = 128: 1 buffer (256 columns) + A -- the MMA waits for each drain.
+// CTA r stages A rows [256 mt + 128 r, +128) and B columns [BN nt + BN/2 r, +BN/2).
 #pragma once
 
 #include <cstdint>
@@ -27,12 +28,13 @@
 
 namespace emu {
 
-template <int MODE>
+template <int MODE, int BN_ = 96>
 struct PairTsCfg {
     static constexpr int BM = 128;                      // A rows per CTA (pair M = 256)
-    static constexpr int BN = 128;                      // pair tile N = D columns per CTA
-    static constexpr int NH = 128;                      // MMA N
-    static constexpr int BNC = 64;                      // B columns staged per CTA
+    static constexpr int BN = BN_;                      // pair tile N = D columns per CTA = MMA N
+    static constexpr int NH = BN;
+    static constexpr int BNC = BN / 2;                  // B columns staged per CTA
+    static constexpr int DBUF = BN <= 96 ? 2 : 1;       // accumulator buffers in TMEM
     static constexpr int BK = 32;
     static constexpr int ESZ = MODE == 0 ? 2 : 4;
     static constexpr int KSTEP = MODE == 0 ? 16 : 8;
@@ -42,17 +44,20 @@ struct PairTsCfg {
     static constexpr uint32_t F32_STAGE = A32_BYTES + B32_BYTES;
     static constexpr uint32_t BOP_BYTES = BNC * BK * ESZ;  // one of B_hi / B_lo
     static constexpr uint32_t OP_STAGE = 2 * BOP_BYTES;
-    static constexpr int S32 = MODE == 0 ? 5 : 4;
-    static constexpr int SOP = 4;
-    static constexpr uint32_t CSTAGE_BYTES = BM * BN * 4;  // 64 KB TMA-store staging
+    static constexpr uint32_t CSTAGE_BYTES = BM * BN * 4;  // TMA-store staging (48 / 64 KB)
     static constexpr uint32_t B_ROW = BK * ESZ;            // 64 (FP16) / 128 (TF32) bytes
     static constexpr uint32_t B_SBO = 8 * B_ROW;
     static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;
-    // TMEM columns: D_hi [0,128), D_corr [128,256); A stages from column 256:
-    // per slot A_hi (ACOLS/2 columns) then A_lo
+    // TMEM columns: buffer b: D_hi [2 BN b, +BN), D_corr [2 BN b + BN, +BN); A stages
+    // from A_COL0: per slot A_hi (ACOLS/2 columns) then A_lo
     static constexpr uint32_t ACOLS = MODE == 0 ? 32 : 64;     // 32 k of hi + lo
-    static constexpr uint32_t A_COL0 = 256;
+    static constexpr uint32_t A_COL0 = DBUF * 2 * BN;
     static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr int SOP = (TMEM_COLS - A_COL0) / ACOLS < 4 ? (TMEM_COLS - A_COL0) / ACOLS : 4;
+    // FP32 stages: as many as fit next to the operand ring and C staging (<= 5)
+    static constexpr int S32_FIT = (232448 - 2048 - SOP * 2 * (BNC * 32 * (MODE == 0 ? 2 : 4)) - BM * BN * 4) /
+                                   (32 * BM * 4 + 32 * BNC * 4);
+    static constexpr int S32 = S32_FIT < 5 ? S32_FIT : 5;
     static constexpr uint32_t KCOLS = MODE == 0 ? 8 : 8;       // TMEM columns per MMA K step
     static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
     static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
@@ -63,6 +68,8 @@ struct PairTsCfg {
     // because the single accumulator buffer makes the MMA wait for it)
     static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 8;
     static constexpr int EPI_WARP0 = 12, NUM_EPI_WARPS = 16;
+    static constexpr int B_THREADS = BNC * 4;                // splitter threads with B work (2 chunks each)
+    static_assert(B_THREADS <= 32 * 8, "B split work");
     static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
     static constexpr int KS = BK / (NUM_SPLIT_WARPS / 4);   // k per splitter warp (A)
     static constexpr int ECOLS = BN / (NUM_EPI_WARPS / 4);  // accumulator columns per combine warp
@@ -70,14 +77,16 @@ struct PairTsCfg {
     static_assert(128 * REGS_CTRL + 32 * NUM_SPLIT_WARPS * REGS_SPLIT + 32 * NUM_EPI_WARPS * REGS_EPI <= 65536,
                   "register budget");
     static_assert(SMEM_BYTES <= 232448, "shared memory");
+    static_assert(SOP >= 2, "TMEM budget for A stages");
+    static_assert(ECOLS % 8 == 0, "combine columns");
 };
 
-template <int MODE, bool RANGE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE>::NUM_THREADS, 1)
+template <int MODE, bool RANGE, int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
 {
-    using Cfg = PairTsCfg<MODE>;
+    using Cfg = PairTsCfg<MODE, BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* f32buf = smem;
@@ -88,8 +97,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     uint64_t* f32_empty = f32_full + Cfg::S32;
     uint64_t* op_full = f32_empty + Cfg::S32;
     uint64_t* op_empty = op_full + Cfg::SOP;
-    uint64_t* acc_full = op_empty + Cfg::SOP;   // [1] (second slot unused)
-    uint64_t* acc_empty = acc_full + 2;         // [1]
+    uint64_t* acc_full = op_empty + Cfg::SOP;   // [DBUF]
+    uint64_t* acc_empty = acc_full + 2;         // [DBUF]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const uint32_t warp = ptx::warp_id();
@@ -155,13 +164,15 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             if (rank == 0 && ptx::elect_one()) {
                 constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 0u, 0u, 256, Cfg::NH);
                 uint32_t s = 0, ph = 0, acc_it = 0;
-                const uint32_t d_hi = tmem_base, d_corr = tmem_base + 128;
                 for (long long t = cid; t < p.num_tiles; t += ncl) {
                     for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                         const int ks0 = kb * p.kb_stages;
                         const int ks1 = min(ks0 + p.kb_stages, nks);
+                        const uint32_t buf = Cfg::DBUF == 2 ? (acc_it & 1u) : 0u;
+                        const uint32_t aph = Cfg::DBUF == 2 ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
+                        const uint32_t d_hi = tmem_base + buf * 2 * Cfg::BN, d_corr = d_hi + Cfg::BN;
                         PROF_T0();
-                        ptx::mbar_wait(&acc_empty[0], (acc_it & 1u) ^ 1u);
+                        ptx::mbar_wait(&acc_empty[buf], aph ^ 1u);
                         PROF_ADD(P_MMA_WAIT_ACC);
                         ptx::tc_fence_after();
                         for (int ks = ks0; ks < ks1; ++ks) {
@@ -198,7 +209,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                             PROF_ADD(P_MMA_ISSUE);
                             if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                         }
-                        ptx::tc_commit_pair(&acc_full[0], 0x3);
+                        ptx::tc_commit_pair(&acc_full[buf], 0x3);
                     }
                 }
             }
@@ -210,7 +221,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t q = warp & 3;                                  // TMEM lane quadrant
         const uint32_t kq = (warp - Cfg::SPLIT_WARP0) >> 2;          // KS-k slice of the stage
         const uint32_t m = q * 32 + lane;                             // A row (TMEM lane)
-        const uint32_t n = tid & 63, quarter = tid >> 6;              // B: 8 k per thread
+        const uint32_t n = tid % Cfg::BNC, quarter = tid / Cfg::BNC;  // B: 8 k per thread (tid < B_THREADS)
+        const bool has_b = tid < Cfg::B_THREADS;
         const uint32_t tq = tmem_base + ((q * 32u) << 16);
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
         uint32_t nonfinite = 0;
@@ -234,9 +246,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll
                 for (int j = 0; j < Cfg::KS; ++j) av[j] = fa[(kq * Cfg::KS + j) * Cfg::BM + m];
                 float4 vb[2];
+                if (has_b) {
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
+                    for (int c = 0; c < 2; ++c)
+                        vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
+                }
                 // ---- A: split into TMEM columns (lane = m)
                 const uint32_t a_hi = tq + Cfg::A_COL0 + sop * Cfg::ACOLS;
                 const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
@@ -260,7 +274,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     }
                 }
                 // ---- B: split into the K-major operand tile in shared memory
-                if (MODE == 0) {
+                if (!has_b) {
+                } else if (MODE == 0) {
                     // one 16-byte FP16 chunk (8 k), K-major SWIZZLE_64B rows
                     uint2 h0, l0, h1, l1;
                     split4_fp16(vb[0], h0, l0);
@@ -310,7 +325,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t q = warp & 3;
         const uint32_t h = e >> 2;                     // column group
         const float scale = MODE == 0 ? (1.0f / 2048.0f) : 1.0f;
-        const uint32_t acc_empty_leader = ptx::mapa_shared(&acc_empty[0], 0);
+        const uint32_t acc_empty_leader = ptx::mapa_shared(&acc_empty[0], 0);   // + 8 * buffer
         uint32_t acc_it = 0;
         for (long long t = cid; t < p.num_tiles; t += ncl) {
             int b, mt, nt;
@@ -319,30 +334,41 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll
             for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
             for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                const uint32_t buf = Cfg::DBUF == 2 ? (acc_it & 1u) : 0u;
+                const uint32_t aph = Cfg::DBUF == 2 ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
                 PROF_T0();
-                ptx::mbar_wait_sleep(&acc_full[0], acc_it & 1u);
+                ptx::mbar_wait(&acc_full[buf], aph);   // on the critical path: spin, do not sleep
                 PROF_ADD(P_EPI_WAIT_ACC);
                 PROF_T0();
                 ptx::tc_fence_after();
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + h * HALF;
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * Cfg::BN + h * HALF;
+                // columns in chunks of 8; CPW chunks loaded per tcgen05.wait::ld
+                constexpr int NCH = HALF / 8, CPW = (HALF <= 24) ? NCH : 2;
 #pragma unroll
-                for (int c = 0; c < HALF / 16; ++c) {
-                    float vh[16], vc[16];
-                    ptx::tmem_ld16(taddr + c * 16, vh);
-                    ptx::tmem_ld16(taddr + 128 + c * 16, vc);
+                for (int c0 = 0; c0 < NCH; c0 += CPW) {
+                    float vh[CPW][8], vc[CPW][8];
+#pragma unroll
+                    for (int c = 0; c < CPW; ++c) {
+                        ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
+                        ptx::tmem_ld8(taddr + Cfg::BN + (c0 + c) * 8, vc[c]);
+                    }
                     ptx::tmem_wait_ld();
-                    if (p.corr) {
 #pragma unroll
-                        for (int j = 0; j < 16; j += 2)
-                            combine2(creg[c * 16 + j], creg[c * 16 + j + 1], vh[j], vh[j + 1], vc[j], vc[j + 1], scale);
-                    } else {
+                    for (int c = 0; c < CPW; ++c) {
+                        float* cr = creg + (c0 + c) * 8;
+                        if (p.corr) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) creg[c * 16 + j] = __fadd_rn(creg[c * 16 + j], vh[j]);
+                            for (int j = 0; j < 8; j += 2)
+                                combine2(cr[j], cr[j + 1], vh[c][j], vh[c][j + 1], vc[c][j], vc[c][j + 1], scale);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) cr[j] = __fadd_rn(cr[j], vh[c][j]);
+                        }
                     }
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader);
+                if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader + 8 * buf);
                 PROF_ADD(P_EPI_DRAIN);
             }
             PROF_T0();

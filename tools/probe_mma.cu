@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
         const uint32_t sb = ptx::smem_u32(smem);
         const uint64_t dA = ptx::smem_desc(sb, 1024, 2048, 2);
         const uint64_t dB = ptx::smem_desc(sb + 16384, 16, 512, 4);
-        const uint32_t d0 = tbase, d1 = tbase + N;                // D_hi, D_corr (N <= 128 for TS)
+        const uint32_t d0 = tbase, d1 = tbase + (N <= 128 ? 128 : N);   // D_hi, D_corr (N <= 128 for TS)
         const uint32_t a_t = tbase + 384;                          // A in TMEM (TS)
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -116,6 +116,11 @@ void run(const char* name)
 
 int main()
 {
+    run<true, true, 96>("pair_ts_m256_n96");
+    run<true, true, 112>("pair_ts_m256_n112");
+    run<true, false, 96>("pair_ss_m256_n96");
+    run<true, false, 112>("pair_ss_m256_n112");
+    run<true, true, 80>("pair_ts_m256_n80");
     run<true, false, 64>("pair_ss_m256_n64");
     run<true, false, 128>("pair_ss_m256_n128");
     run<true, false, 256>("pair_ss_m256_n256");
