@@ -28,13 +28,15 @@
 
 namespace emu {
 
-template <int MODE, int BN_ = 96>
+template <int MODE, int BN_ = 96, int HALVES_ = 1>
 struct PairTsCfg {
     static constexpr int BM = 128;                      // A rows per CTA (pair M = 256)
-    static constexpr int BN = BN_;                      // pair tile N = D columns per CTA = MMA N
-    static constexpr int NH = BN;
+    static constexpr int BN = BN_;                      // pair tile N = D columns per CTA
+    static constexpr int HALVES = HALVES_;              // accumulator column halves (own barriers)
+    static constexpr int NH = BN / HALVES;              // MMA N
     static constexpr int BNC = BN / 2;                  // B columns staged per CTA
-    static constexpr int DBUF = BN <= 96 ? 2 : 1;       // accumulator buffers in TMEM
+    static constexpr int DBUF = (BN <= 96 && HALVES == 1) ? 2 : 1;   // accumulator buffers in TMEM
+    static constexpr int NUNIT = DBUF * HALVES;         // (D_hi, D_corr) units of NH columns
     static constexpr int BK = 32;
     static constexpr int ESZ = MODE == 0 ? 2 : 4;
     static constexpr int KSTEP = MODE == 0 ? 16 : 8;
@@ -48,10 +50,10 @@ struct PairTsCfg {
     static constexpr uint32_t B_ROW = BK * ESZ;            // 64 (FP16) / 128 (TF32) bytes
     static constexpr uint32_t B_SBO = 8 * B_ROW;
     static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;
-    // TMEM columns: buffer b: D_hi [2 BN b, +BN), D_corr [2 BN b + BN, +BN); A stages
+    // TMEM columns: unit u: D_hi [2 NH u, +NH), D_corr [2 NH u + NH, +NH); A stages
     // from A_COL0: per slot A_hi (ACOLS/2 columns) then A_lo
     static constexpr uint32_t ACOLS = MODE == 0 ? 32 : 64;     // 32 k of hi + lo
-    static constexpr uint32_t A_COL0 = DBUF * 2 * BN;
+    static constexpr uint32_t A_COL0 = NUNIT * 2 * NH;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int SOP = (TMEM_COLS - A_COL0) / ACOLS < 4 ? (TMEM_COLS - A_COL0) / ACOLS : 4;
     // FP32 stages: as many as fit next to the operand ring and C staging (<= 5)
@@ -81,12 +83,12 @@ struct PairTsCfg {
     static_assert(ECOLS % 8 == 0, "combine columns");
 };
 
-template <int MODE, bool RANGE, int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN>::NUM_THREADS, 1)
+template <int MODE, bool RANGE, int BN, int HALVES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, HALVES>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
 {
-    using Cfg = PairTsCfg<MODE, BN>;
+    using Cfg = PairTsCfg<MODE, BN, HALVES>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* f32buf = smem;
@@ -121,7 +123,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&acc_full[i], 1);
-            ptx::mbar_init(&acc_empty[i], 2 * Cfg::NUM_EPI_WARPS);
+            ptx::mbar_init(&acc_empty[i], 2 * Cfg::NUM_EPI_WARPS / Cfg::HALVES);
         }
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmA);
@@ -153,8 +155,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                         ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
                         ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab);
-                        ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
-                                                nt * Cfg::BN + rank * Cfg::BNC, bb);
+#pragma unroll
+                        for (int h = 0; h < Cfg::HALVES; ++h)   // CTA r: columns [NH h + NH/2 r, +NH/2) of each half
+                            ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES + h * (Cfg::BNC / Cfg::HALVES) * 128, &tmB,
+                                                    &f32_full[s], ks * Cfg::BK,
+                                                    nt * Cfg::BN + h * Cfg::NH + rank * (Cfg::NH / 2), bb);
                         if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                     }
                 }
@@ -163,53 +168,66 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             // -------------------------------------------- MMA issuer (leader CTA only)
             if (rank == 0 && ptx::elect_one()) {
                 constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 0u, 0u, 256, Cfg::NH);
-                uint32_t s = 0, ph = 0, acc_it = 0;
+                uint32_t s0 = 0, ph0 = 0, acc_it = 0;
                 for (long long t = cid; t < p.num_tiles; t += ncl) {
                     for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                         const int ks0 = kb * p.kb_stages;
                         const int ks1 = min(ks0 + p.kb_stages, nks);
-                        const uint32_t buf = Cfg::DBUF == 2 ? (acc_it & 1u) : 0u;
-                        const uint32_t aph = Cfg::DBUF == 2 ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
-                        const uint32_t d_hi = tmem_base + buf * 2 * Cfg::BN, d_corr = d_hi + Cfg::BN;
-                        PROF_T0();
-                        ptx::mbar_wait(&acc_empty[buf], aph ^ 1u);
-                        PROF_ADD(P_MMA_WAIT_ACC);
-                        ptx::tc_fence_after();
-                        for (int ks = ks0; ks < ks1; ++ks) {
+                        uint32_t s = s0, ph = ph0;
+                        // HALVES == 2: all MMAs of column half 0 for the k-block, commit its
+                        // accumulator, then half 1 -- the drain of half 0 overlaps half 1's MMAs.
+                        // The k-block's operand slots stay resident until half 1 is issued.
+#pragma unroll 1
+                        for (int h = 0; h < Cfg::HALVES; ++h) {
+                            const uint32_t unit = Cfg::HALVES == 2 ? (uint32_t)h
+                                                : (Cfg::DBUF == 2 ? (acc_it & 1u) : 0u);
+                            const uint32_t aph = (Cfg::DBUF == 2) ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
+                            const uint32_t d_hi = tmem_base + unit * 2 * Cfg::NH, d_corr = d_hi + Cfg::NH;
                             PROF_T0();
-                            ptx::mbar_wait(&op_full[s], ph);
-                            PROF_ADD(P_MMA_WAIT_OP);
-                            PROF_T0();
+                            ptx::mbar_wait(&acc_empty[unit], aph ^ 1u);
+                            PROF_ADD(P_MMA_WAIT_ACC);
                             ptx::tc_fence_after();
-                            const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
-                            const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
-                            const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+                            s = s0; ph = ph0;
+                            for (int ks = ks0; ks < ks1; ++ks) {
+                                if (h == 0) {
+                                    PROF_T0();
+                                    ptx::mbar_wait(&op_full[s], ph);
+                                    PROF_ADD(P_MMA_WAIT_OP);
+                                    ptx::tc_fence_after();
+                                }
+                                PROF_T0();
+                                const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
+                                const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                                const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE) +
+                                                       h * (Cfg::BNC / Cfg::HALVES) * Cfg::B_ROW;
 #pragma unroll
-                            for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
-                                                                      Cfg::B_SBO, Cfg::B_LAYOUT);
-                                const uint32_t ka = st * Cfg::KCOLS;
-                                const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
-                                if (MODE == 0) {
-                                    ptx::mma_f16_pair_ts(d_hi, a_hi + ka, dB_hi, idesc, acc);        // P1
-                                    if (p.corr) {
-                                        ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);  // P2
-                                        ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);   // P3
-                                    }
-                                } else {
-                                    ptx::mma_tf32_pair_ts(d_hi, a_hi + ka, dB_hi, idesc, acc);
-                                    if (p.corr) {
-                                        ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
-                                        ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
+                                for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                    const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                    const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
+                                                                          Cfg::B_SBO, Cfg::B_LAYOUT);
+                                    const uint32_t ka = st * Cfg::KCOLS;
+                                    const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                    if (MODE == 0) {
+                                        ptx::mma_f16_pair_ts(d_hi, a_hi + ka, dB_hi, idesc, acc);        // P1
+                                        if (p.corr) {
+                                            ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);  // P2
+                                            ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);   // P3
+                                        }
+                                    } else {
+                                        ptx::mma_tf32_pair_ts(d_hi, a_hi + ka, dB_hi, idesc, acc);
+                                        if (p.corr) {
+                                            ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
+                                            ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
+                                        }
                                     }
                                 }
+                                if (h == Cfg::HALVES - 1) ptx::tc_commit_pair(&op_empty[s], 0x3);   // slot free
+                                PROF_ADD(P_MMA_ISSUE);
+                                if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                             }
-                            ptx::tc_commit_pair(&op_empty[s], 0x3);   // slot free (both CTAs)
-                            PROF_ADD(P_MMA_ISSUE);
-                            if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                            ptx::tc_commit_pair(&acc_full[unit], 0x3);
                         }
-                        ptx::tc_commit_pair(&acc_full[buf], 0x3);
+                        s0 = s; ph0 = ph;
                     }
                 }
             }
@@ -323,7 +341,10 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         constexpr int HALF = Cfg::ECOLS;               // this warp's accumulator columns
         const uint32_t e = warp - Cfg::EPI_WARP0;
         const uint32_t q = warp & 3;
-        const uint32_t h = e >> 2;                     // column group
+        const uint32_t h = e >> 2;                     // column group: tile columns [HALF h, +HALF)
+        // accumulator unit holding those columns (HALVES == 2: the column half)
+        const uint32_t my_half = Cfg::HALVES == 2 ? (h * HALF) / Cfg::NH : 0u;
+        const uint32_t col_in_unit = h * HALF - my_half * Cfg::NH;
         const float scale = MODE == 0 ? (1.0f / 2048.0f) : 1.0f;
         const uint32_t acc_empty_leader = ptx::mapa_shared(&acc_empty[0], 0);   // + 8 * buffer
         uint32_t acc_it = 0;
@@ -334,14 +355,14 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll
             for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
             for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
-                const uint32_t buf = Cfg::DBUF == 2 ? (acc_it & 1u) : 0u;
+                const uint32_t buf = Cfg::HALVES == 2 ? my_half : (Cfg::DBUF == 2 ? (acc_it & 1u) : 0u);
                 const uint32_t aph = Cfg::DBUF == 2 ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
                 PROF_T0();
                 ptx::mbar_wait(&acc_full[buf], aph);   // on the critical path: spin, do not sleep
                 PROF_ADD(P_EPI_WAIT_ACC);
                 PROF_T0();
                 ptx::tc_fence_after();
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * Cfg::BN + h * HALF;
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * Cfg::NH + col_in_unit;
                 // columns in chunks of 8; CPW chunks loaded per tcgen05.wait::ld
                 constexpr int NCH = HALF / 8, CPW = (HALF <= 24) ? NCH : 2;
 #pragma unroll
@@ -350,7 +371,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll
                     for (int c = 0; c < CPW; ++c) {
                         ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
-                        ptx::tmem_ld8(taddr + Cfg::BN + (c0 + c) * 8, vc[c]);
+                        ptx::tmem_ld8(taddr + Cfg::NH + (c0 + c) * 8, vc[c]);
                     }
                     ptx::tmem_wait_ld();
 #pragma unroll

@@ -65,11 +65,13 @@ def main():
     tot = v["cta_total"] / ctas
     print(f"{cfg} mode={mode} {ms:.3f} ms/launch, {2.0 * m * n * k * batch / ms / 1e9:.1f} TF; "
           f"cycles per CTA {tot:.0f}")
-    nspl = 8 if os.environ.get("EMU_KERNEL") == "single" or m <= 128 else 16
+    kern = os.environ.get("EMU_KERNEL", "ts")
+    nspl = 8 if kern in ("single", "ts") or m <= 128 else 16
+    nepi = 16 if kern == "ts" and m > 128 else 8
     ctas_mma = ctas if nspl == 8 else ctas // 2     # pair kernels: the MMA issuer lives in the leader CTA
     per = {"prod_wait_empty": 1, "mma_wait_acc": ctas_mma / ctas, "mma_wait_op": ctas_mma / ctas,
            "mma_issue": ctas_mma / ctas, "spl_wait_f32": nspl, "spl_wait_op": nspl, "spl_work": nspl,
-           "epi_wait_acc": 8, "epi_drain": 8, "epi_store": 8}
+           "epi_wait_acc": nepi, "epi_drain": nepi, "epi_store": nepi}
     for k_, nw in per.items():
         print(f"  {k_:16s} {v[k_] / ctas / nw / tot * 100:6.1f}% of CTA time (per warp)")
 
