@@ -45,7 +45,7 @@ struct DeviceInfo {
     int sms = 0;
     bool attr_set[32] = {};
     bool pair_attr_set[16] = {};
-    bool ts_attr_set[16] = {};
+    bool ts_attr_set[32] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -311,18 +311,18 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
-template <int MODE, bool RANGE, int BN, int HALVES>
+template <int MODE, bool RANGE, int BN, int HALVES, bool SPLITC>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
                          unsigned flags)
 {
-    using Cfg = emu::PairTsCfg<MODE, BN, HALVES>;
+    using Cfg = emu::PairTsCfg<MODE, BN, HALVES, SPLITC>;
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        const int slot = ((MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1)) * 2 + (HALVES - 1);
+        const int slot = (((MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1)) * 2 + (HALVES - 1)) * 2 + (SPLITC ? 1 : 0);
         if (!g_dev[dev].ts_attr_set[slot]) {
-            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, HALVES>,
+            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, HALVES, SPLITC>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
                 return EMU_STATUS_CUDA_ERROR;
             g_dev[dev].ts_attr_set[slot] = true;
@@ -373,7 +373,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
-    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, HALVES>
+    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, HALVES, SPLITC>
         <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
@@ -455,26 +455,27 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     const bool ts = !ldg && (kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     const int kbs = (kblock > 0 ? kblock : 64) / 32;
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
-    // tile width of the TS kernel (profiles/r01_summary.md): 128 (one accumulator
-    // buffer) for FP16 and short-k TF32; 96 (two buffers, the MMA never waits for a
-    // drain) for long-k TF32, whose MMAs are long enough to hide the extra A split.
+    // tile width of the TS kernel (profiles/r01_summary.md): 128 with one accumulator
+    // buffer whose D_corr and D_hi drains overlap the other part's MMAs (SPLITC); the
+    // double-buffered 96-wide tile (EMU_TS_N=96) and the plain single buffer
+    // (EMU_TS_SPLITC=0) stay selectable for comparison.
     static const int ts_n_env = env_int("EMU_TS_N", 0, 0, 128);   // tuning only
-    static const int ts_h_env = env_int("EMU_TS_HALVES", 0, 0, 2);   // tuning only
-    const int ts_n = ts_n_env ? ts_n_env : ((mode == EMU_SPLIT_FP16 || k <= 512) ? 128 : 96);
-    const int ts_h = ts_n == 96 ? 1 : (ts_h_env ? ts_h_env : 1);
-    const bool ts_halves_ok = kbs <= emu::PairTsCfg<0, 128, 2>::SOP && kbs <= emu::PairTsCfg<1, 128, 2>::SOP;
+    const int ts_n = ts_n_env ? ts_n_env : 128;
+    static const int ts_sc_env = env_int("EMU_TS_SPLITC", 1, 0, 1);   // tuning only (default on)
+    const bool ts_sc = ts_n == 128 && ts_sc_env;
 #define EMU_RUN_TS(MODE_, RANGE_)                                                                                      \
     do {                                                                                                               \
-        if (ts_n == 128 && ts_h == 2 && ts_halves_ok)                                                                  \
-            return run_gemm_pair_ts<MODE_, RANGE_, 128, 2>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,          \
-                                                           strideB, beta, C, ldc, strideC, batch, s, d_range_flag,     \
-                                                           kblock, flags);                                             \
+        if (ts_sc)                                                                                                     \
+            return run_gemm_pair_ts<MODE_, RANGE_, 128, 1, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,    \
+                                                                 strideB, beta, C, ldc, strideC, batch, s,             \
+                                                                 d_range_flag, kblock, flags);                         \
         if (ts_n == 128)                                                                                               \
-            return run_gemm_pair_ts<MODE_, RANGE_, 128, 1>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,          \
-                                                           strideB, beta, C, ldc, strideC, batch, s, d_range_flag,     \
-                                                           kblock, flags);                                             \
-        return run_gemm_pair_ts<MODE_, RANGE_, 96, 1>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB,      \
-                                                      beta, C, ldc, strideC, batch, s, d_range_flag, kblock, flags);   \
+            return run_gemm_pair_ts<MODE_, RANGE_, 128, 1, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,   \
+                                                                  strideB, beta, C, ldc, strideC, batch, s,            \
+                                                                  d_range_flag, kblock, flags);                        \
+        return run_gemm_pair_ts<MODE_, RANGE_, 96, 1, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,        \
+                                                             strideB, beta, C, ldc, strideC, batch, s, d_range_flag,   \
+                                                             kblock, flags);                                           \
     } while (0)
     if (ts) {
         if (mode == EMU_SPLIT_FP16) {

@@ -28,7 +28,7 @@
 
 namespace emu {
 
-template <int MODE, int BN_ = 96, int HALVES_ = 1>
+template <int MODE, int BN_ = 96, int HALVES_ = 1, bool SPLITC_ = false>
 struct PairTsCfg {
     static constexpr int BM = 128;                      // A rows per CTA (pair M = 256)
     static constexpr int BN = BN_;                      // pair tile N = D columns per CTA
@@ -55,7 +55,10 @@ struct PairTsCfg {
     static constexpr uint32_t ACOLS = MODE == 0 ? 32 : 64;     // 32 k of hi + lo
     static constexpr uint32_t A_COL0 = NUNIT * 2 * NH;
     static constexpr uint32_t TMEM_COLS = 512;
-    static constexpr int SOP = (TMEM_COLS - A_COL0) / ACOLS < 4 ? (TMEM_COLS - A_COL0) / ACOLS : 4;
+    // operand slots: as many A stages as TMEM holds (column halves keep a k-block's
+    // slots resident across both halves, so they need more slots to run ahead)
+    static constexpr int SOP_MAX = HALVES == 2 ? 8 : 4;
+    static constexpr int SOP = (TMEM_COLS - A_COL0) / ACOLS < SOP_MAX ? (TMEM_COLS - A_COL0) / ACOLS : SOP_MAX;
     // FP32 stages: as many as fit next to the operand ring and C staging (<= 5)
     static constexpr int S32_FIT = (232448 - 2048 - SOP * 2 * (BNC * 32 * (MODE == 0 ? 2 : 4)) - BM * BN * 4) /
                                    (32 * BM * 4 + 32 * BNC * 4);
@@ -75,7 +78,11 @@ struct PairTsCfg {
     static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
     static constexpr int KS = BK / (NUM_SPLIT_WARPS / 4);   // k per splitter warp (A)
     static constexpr int ECOLS = BN / (NUM_EPI_WARPS / 4);  // accumulator columns per combine warp
-    static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = 64, REGS_EPI = 80;
+    // single buffer: the correction products and P1 get their own full/empty barriers, so
+    // the drain of D_corr overlaps P1 and the drain of D_hi overlaps the next k-block's
+    // correction products (no extra TMEM; the combine holds one part in registers)
+    static constexpr bool SPLITC = SPLITC_ && DBUF == 1 && HALVES == 1;
+    static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = SPLITC ? 56 : 64, REGS_EPI = SPLITC ? 88 : 80;
     static_assert(128 * REGS_CTRL + 32 * NUM_SPLIT_WARPS * REGS_SPLIT + 32 * NUM_EPI_WARPS * REGS_EPI <= 65536,
                   "register budget");
     static_assert(SMEM_BYTES <= 232448, "shared memory");
@@ -83,12 +90,12 @@ struct PairTsCfg {
     static_assert(ECOLS % 8 == 0, "combine columns");
 };
 
-template <int MODE, bool RANGE, int BN, int HALVES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, HALVES>::NUM_THREADS, 1)
+template <int MODE, bool RANGE, int BN, int HALVES, bool SPLITC_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, HALVES, SPLITC_>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
 {
-    using Cfg = PairTsCfg<MODE, BN, HALVES>;
+    using Cfg = PairTsCfg<MODE, BN, HALVES, SPLITC_>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* f32buf = smem;
@@ -169,6 +176,74 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             if (rank == 0 && ptx::elect_one()) {
                 constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 0u, 0u, 256, Cfg::NH);
                 uint32_t s0 = 0, ph0 = 0, acc_it = 0;
+                if constexpr (Cfg::SPLITC) {
+                    // per k-block: P2 + P3 into D_corr (barrier pair 1), then P1 into D_hi (pair 0)
+                    for (long long t = cid; t < p.num_tiles; t += ncl) {
+                        for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                            const int ks0 = kb * p.kb_stages;
+                            const int ks1 = min(ks0 + p.kb_stages, nks);
+                            const uint32_t aph = acc_it & 1u;
+                            const uint32_t d_hi = tmem_base, d_corr = tmem_base + Cfg::NH;
+                            PROF_T0();
+                            ptx::mbar_wait(&acc_empty[1], aph ^ 1u);
+                            PROF_ADD(P_MMA_WAIT_ACC);
+                            ptx::tc_fence_after();
+                            uint32_t s = s0, ph = ph0;
+                            for (int ks = ks0; ks < ks1; ++ks) {
+                                PROF_T0();
+                                ptx::mbar_wait(&op_full[s], ph);
+                                PROF_ADD(P_MMA_WAIT_OP);
+                                ptx::tc_fence_after();
+                                PROF_T0();
+                                if (p.corr) {
+                                    const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
+                                    const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                                    for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                        const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
+                                                                              Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint32_t ka = st * Cfg::KCOLS;
+                                        const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                        if (MODE == 0) {
+                                            ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);   // P2
+                                            ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);    // P3
+                                        } else {
+                                            ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
+                                            ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
+                                        }
+                                    }
+                                }
+                                PROF_ADD(P_MMA_ISSUE);
+                                if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                            }
+                            ptx::tc_commit_pair(&acc_full[1], 0x3);
+                            PROF_T0();
+                            ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
+                            PROF_ADD(P_MMA_WAIT_ACC);
+                            ptx::tc_fence_after();
+                            PROF_T0();
+                            s = s0; ph = ph0;
+                            for (int ks = ks0; ks < ks1; ++ks) {
+                                const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
+                                const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                                for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                    const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                    const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                    if (MODE == 0) ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
+                                    else ptx::mma_tf32_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);
+                                }
+                                ptx::tc_commit_pair(&op_empty[s], 0x3);   // slot free
+                                if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                            }
+                            ptx::tc_commit_pair(&acc_full[0], 0x3);
+                            PROF_ADD(P_MMA_ISSUE);
+                            s0 = s; ph0 = ph;
+                        }
+                    }
+                } else
                 for (long long t = cid; t < p.num_tiles; t += ncl) {
                     for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                         const int ks0 = kb * p.kb_stages;
@@ -354,6 +429,61 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             float creg[HALF];
 #pragma unroll
             for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
+            if constexpr (Cfg::SPLITC) {
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + h * HALF;
+                const uint32_t emp_hi = ptx::mapa_shared(&acc_empty[0], 0), emp_corr = emp_hi + 8;
+                for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                    const uint32_t aph = acc_it & 1u;
+                    // D_corr first (P2 + P3 are issued first); hold it while P1 runs
+                    PROF_T0();
+                    ptx::mbar_wait(&acc_full[1], aph);
+                    PROF_ADD(P_EPI_WAIT_ACC);
+                    PROF_T0();
+                    ptx::tc_fence_after();
+                    float vc[HALF / 8][8];
+                    if (p.corr) {
+#pragma unroll
+                        for (int c = 0; c < HALF / 8; ++c) ptx::tmem_ld8(taddr + Cfg::NH + c * 8, vc[c]);
+                        ptx::tmem_wait_ld();
+                    }
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(emp_corr);
+                    PROF_ADD(P_EPI_DRAIN);
+                    PROF_T0();
+                    ptx::mbar_wait(&acc_full[0], aph);
+                    PROF_ADD(P_EPI_WAIT_ACC);
+                    PROF_T0();
+                    ptx::tc_fence_after();
+                    constexpr int CPW = 2;
+#pragma unroll
+                    for (int c0 = 0; c0 < HALF / 8; c0 += CPW) {
+                        float vh[CPW][8];
+#pragma unroll
+                        for (int c = 0; c < CPW; ++c) ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
+                        ptx::tmem_wait_ld();
+                        if (c0 + CPW >= HALF / 8) {   // last chunk read: release D_hi before the math
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive_cluster(emp_hi);
+                        }
+#pragma unroll
+                        for (int c = 0; c < CPW; ++c) {
+                            float* cr = creg + (c0 + c) * 8;
+                            const float* cc = vc[c0 + c];
+                            if (p.corr) {
+#pragma unroll
+                                for (int j = 0; j < 8; j += 2)
+                                    combine2(cr[j], cr[j + 1], vh[c][j], vh[c][j + 1], cc[j], cc[j + 1], scale);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) cr[j] = __fadd_rn(cr[j], vh[c][j]);
+                            }
+                        }
+                    }
+                    PROF_ADD(P_EPI_DRAIN);
+                }
+            } else
             for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                 const uint32_t buf = Cfg::HALVES == 2 ? my_half : (Cfg::DBUF == 2 ? (acc_it & 1u) : 0u);
                 const uint32_t aph = Cfg::DBUF == 2 ? ((acc_it >> 1) & 1u) : (acc_it & 1u);

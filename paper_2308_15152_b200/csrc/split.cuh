@@ -48,8 +48,42 @@ __device__ __forceinline__ void sub_mul2048_f32x2(float x0, float x1, float h0, 
         : "=f"(r0), "=f"(r1) : "f"(x0), "f"(x1), "f"(h0), "f"(h1), "f"(2048.0f));
 }
 
-// Eqs. corr-1/corr-2 for two elements: packed hi and packed lo (low half = x0)
+// x - toFP32(h) for both halves of a packed binary16 pair with the mixed-precision
+// FMA (fma.rn.f32.f16: h * (-1) + x, one FHFMA per element, no separate unpack).
+// The exact difference x - h is representable, so this equals __fsub_rn(x, h).
+__device__ __forceinline__ void sub_f16x2_from_f32x2(uint32_t h, float x0, float x1, float& r0, float& r1)
+{
+    asm("{\n\t.reg .f16 a, b, m;\n\t"
+        "mov.b32 {a, b}, %2;\n\t"
+        "mov.b16 m, 0xBC00;\n\t"
+        "fma.rn.f32.f16 %0, a, m, %3;\n\t"
+        "fma.rn.f32.f16 %1, b, m, %4;\n\t}"
+        : "=f"(r0), "=f"(r1) : "r"(h), "f"(x0), "f"(x1));
+}
+
+__device__ __forceinline__ void mul2048_f32x2(float& r0, float& r1)
+{
+    asm("{\n\t.reg .b64 d, b;\n\t"
+        "mov.b64 d, {%0, %1};\n\t"
+        "mov.b64 b, {%2, %2};\n\t"
+        "mul.rn.f32x2 d, d, b;\n\t"
+        "mov.b64 {%0, %1}, d;\n\t}"
+        : "+f"(r0), "+f"(r1) : "f"(2048.0f));
+}
+
+// Eqs. corr-1/corr-2 for two elements: packed hi and packed lo (low half = x0).
+// Per element: 1/2 F2FP (hi), 1 FHFMA (x - hi), 1/2 FMUL2 (* 2^11), 1/2 F2FP (lo).
 __device__ __forceinline__ void split_fp16x2(float x0, float x1, uint32_t& hi, uint32_t& lo)
+{
+    hi = f32x2_to_f16x2_rn(x0, x1);
+    float r0, r1;
+    sub_f16x2_from_f32x2(hi, x0, x1, r0, r1);
+    mul2048_f32x2(r0, r1);
+    lo = f32x2_to_f16x2_rn(r0, r1);
+}
+
+// the earlier form (unpack hi to FP32, FADD2, FMUL2) -- kept for the tools' A/B
+__device__ __forceinline__ void split_fp16x2_unpack(float x0, float x1, uint32_t& hi, uint32_t& lo)
 {
     hi = f32x2_to_f16x2_rn(x0, x1);
     float h0, h1;

@@ -6,7 +6,7 @@ python -c "import oracle; oracle.build()"
 EMU_TS_HALVES=2 timeout 120 python tools/dbg_small.py > gpurun_out/dbg_$TAG.log 2>&1; RC=$?; echo "dbg rc=$RC" >> gpurun_out/dbg_$TAG.log
 if [ $RC -ne 0 ]; then echo "dbg failed rc=$RC"; exit 1; fi
 EMU_TS_HALVES=2 timeout 900 python -m pytest tests/test_gpu_gemm.py -q -x > gpurun_out/pytest_gemm_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gemm_$TAG.log
-for H in 1 2; do for mode in fp16 tf32; do
+for H in ${HS:-1 2}; do for mode in fp16 tf32; do
   EMU_TS_HALVES=$H EMU_TS_N=128 timeout 300 python bench.py --steps 300 --warmup 10 --mode $mode --no-cpu-baseline --no-e2e > gpurun_out/bench_c2_${mode}_h${H}_$TAG.log 2>&1
   EMU_TS_HALVES=$H EMU_TS_N=128 timeout 300 python bench.py --steps 5 --warmup 3 --mode $mode --config c3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_${mode}_h${H}_$TAG.log 2>&1
 done; done
