@@ -311,18 +311,19 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
-template <int MODE, bool RANGE, int BN, int HALVES, bool SPLITC>
+template <int MODE, bool RANGE, int BN, bool SPLITC, bool ASTAT>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
                          unsigned flags)
 {
-    using Cfg = emu::PairTsCfg<MODE, BN, HALVES, SPLITC>;
+    using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT>;
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        const int slot = (((MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1)) * 2 + (HALVES - 1)) * 2 + (SPLITC ? 1 : 0);
+        const int slot = (((MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1)) * 2 + (SPLITC ? 1 : 0)) * 2 +
+                         (ASTAT ? 1 : 0);
         if (!g_dev[dev].ts_attr_set[slot]) {
-            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, HALVES, SPLITC>,
+            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
                 return EMU_STATUS_CUDA_ERROR;
             g_dev[dev].ts_attr_set[slot] = true;
@@ -340,7 +341,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     if (!make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA, Cfg::BM, Cfg::BK,
                   CU_TENSOR_MAP_SWIZZLE_NONE))
         return EMU_STATUS_NOT_SUPPORTED;
-    if (!make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB, Cfg::BK, Cfg::BNC / Cfg::HALVES,
+    if (!make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB, Cfg::BK, Cfg::BNC,
                   CU_TENSOR_MAP_SWIZZLE_128B))
         return EMU_STATUS_NOT_SUPPORTED;
     int tma_store = beta == 0.0f && aligned16(C) && ldc % 4 == 0 && (!c_b || strideC % 4 == 0) &&
@@ -372,8 +373,11 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
         p.l2_policy = pol;
     }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
-    const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
-    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, HALVES, SPLITC>
+    p.num_units = ASTAT ? (long long)p.tiles_m * batch : p.num_tiles;
+    p.unit_tiles = ASTAT ? p.tiles_n : 1;
+    if (ASTAT && p.num_k_stages > Cfg::ASLOTS) return EMU_STATUS_NOT_SUPPORTED;   // dispatch guarantees it
+    const long long clusters = std::min<long long>(p.num_units, sms / 2);
+    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT>
         <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
@@ -453,7 +457,6 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     // with more than one 128-row block; the SMEM-operand pair kernel stays selectable
     // (EMU_KERNEL=pair) for comparison.
     const bool ts = !ldg && (kernel_pref == 3 || (kernel_pref == 0 && m > 128));
-    const int kbs = (kblock > 0 ? kblock : 64) / 32;
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     // tile width of the TS kernel (profiles/r01_summary.md): 128 with one accumulator
     // buffer whose D_corr and D_hi drains overlap the other part's MMAs (SPLITC); the
@@ -462,20 +465,32 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     static const int ts_n_env = env_int("EMU_TS_N", 0, 0, 128);   // tuning only
     const int ts_n = ts_n_env ? ts_n_env : 128;
     static const int ts_sc_env = env_int("EMU_TS_SPLITC", 1, 0, 1);   // tuning only (default on)
+    static const int ts_as_env = env_int("EMU_TS_ASTAT", 1, 0, 1);    // tuning only (default on)
     const bool ts_sc = ts_n == 128 && ts_sc_env;
+    // A-stationary: all of k fits the TMEM A slots, at least two n-tiles share the split
+    // A, and there are enough (batch, m-pair) row blocks to keep every cluster busy
+    const long long ts_units = (long long)((m + 255) / 256) * batch;
+    const int ts_aslots = mode == EMU_SPLIT_FP16 ? emu::PairTsCfg<0, 128, true, true>::ASLOTS
+                                                 : emu::PairTsCfg<1, 128, true, true>::ASLOTS;
+    const bool ts_as = ts_sc && ts_as_env && (k + 31) / 32 <= ts_aslots && (n + 127) / 128 >= 2 &&
+                       ts_units >= 2LL * (sms / 2);
 #define EMU_RUN_TS(MODE_, RANGE_)                                                                                      \
     do {                                                                                                               \
+        if (ts_as)                                                                                                     \
+            return run_gemm_pair_ts<MODE_, RANGE_, 128, true, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, \
+                                                                    strideB, beta, C, ldc, strideC, batch, s,          \
+                                                                    d_range_flag, kblock, flags);                      \
         if (ts_sc)                                                                                                     \
-            return run_gemm_pair_ts<MODE_, RANGE_, 128, 1, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,    \
+            return run_gemm_pair_ts<MODE_, RANGE_, 128, true, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,     \
+                                                                     ldb, strideB, beta, C, ldc, strideC, batch, s,    \
+                                                                     d_range_flag, kblock, flags);                     \
+        if (ts_n == 128)                                                                                               \
+            return run_gemm_pair_ts<MODE_, RANGE_, 128, false, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,    \
+                                                                      ldb, strideB, beta, C, ldc, strideC, batch, s,   \
+                                                                      d_range_flag, kblock, flags);                    \
+        return run_gemm_pair_ts<MODE_, RANGE_, 96, false, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,    \
                                                                  strideB, beta, C, ldc, strideC, batch, s,             \
                                                                  d_range_flag, kblock, flags);                         \
-        if (ts_n == 128)                                                                                               \
-            return run_gemm_pair_ts<MODE_, RANGE_, 128, 1, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,   \
-                                                                  strideB, beta, C, ldc, strideC, batch, s,            \
-                                                                  d_range_flag, kblock, flags);                        \
-        return run_gemm_pair_ts<MODE_, RANGE_, 96, 1, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,        \
-                                                             strideB, beta, C, ldc, strideC, batch, s, d_range_flag,   \
-                                                             kblock, flags);                                           \
     } while (0)
     if (ts) {
         if (mode == EMU_SPLIT_FP16) {

@@ -12,10 +12,17 @@
 // Tile (per cluster of two CTAs): 256 (m) x BN (n); MMA cta_group::2, M = 256,
 // N = BN per instruction (tools/probe_mma: A-from-TMEM MMAs run at the full
 // tensor rate for any N multiple of 16).  TMEM per CTA: DBUF accumulator buffers
-// of (D_hi, D_corr) x BN columns, then SOP A stages:
-//   BN =  96: 2 buffers (384 columns) + A -- the MMA of k-block j+1 overlaps the
-//             drain of k-block j (the default);
-//   BN = 128: 1 buffer (256 columns) + A -- the MMA waits for each drain.
+// of (D_hi, D_corr) x BN columns, then the A stages:
+//   BN = 128 (default): 1 buffer (256 columns).  With SPLITC the correction
+//             products (P2, P3 -> D_corr) and P1 (-> D_hi) of a k-block have their
+//             own full/empty barriers, so the drain of D_corr overlaps P1 and the
+//             drain of D_hi overlaps the next k-block's P2/P3;
+//   BN =  96: 2 buffers (384 columns) -- the MMA of k-block j+1 overlaps the
+//             drain of k-block j (kept for comparison, EMU_TS_N=96).
+// A-stationary (ASTAT, short k): the split A of a whole (batch item, 256-row block)
+// -- all k, hi and lo -- stays in TMEM (k <= 256 FP16, k <= 128 TF32) while the
+// cluster walks every n-tile of that row block, so A is loaded and split once per
+// row block instead of once per n-tile (c2: a third less splitter work).
 // CTA r stages A rows [256 mt + 128 r, +128) and B columns [BN nt + BN/2 r, +BN/2).
 #pragma once
 
@@ -28,15 +35,14 @@
 
 namespace emu {
 
-template <int MODE, int BN_ = 96, int HALVES_ = 1, bool SPLITC_ = false>
+template <int MODE, int BN_ = 128, bool SPLITC_ = true, bool ASTAT_ = false>
 struct PairTsCfg {
     static constexpr int BM = 128;                      // A rows per CTA (pair M = 256)
     static constexpr int BN = BN_;                      // pair tile N = D columns per CTA
-    static constexpr int HALVES = HALVES_;              // accumulator column halves (own barriers)
-    static constexpr int NH = BN / HALVES;              // MMA N
     static constexpr int BNC = BN / 2;                  // B columns staged per CTA
-    static constexpr int DBUF = (BN <= 96 && HALVES == 1) ? 2 : 1;   // accumulator buffers in TMEM
-    static constexpr int NUNIT = DBUF * HALVES;         // (D_hi, D_corr) units of NH columns
+    static constexpr int DBUF = BN <= 96 ? 2 : 1;       // accumulator buffers in TMEM
+    static constexpr bool SPLITC = SPLITC_ && DBUF == 1;
+    static constexpr bool ASTAT = ASTAT_ && SPLITC;
     static constexpr int BK = 32;
     static constexpr int ESZ = MODE == 0 ? 2 : 4;
     static constexpr int KSTEP = MODE == 0 ? 16 : 8;
@@ -50,27 +56,25 @@ struct PairTsCfg {
     static constexpr uint32_t B_ROW = BK * ESZ;            // 64 (FP16) / 128 (TF32) bytes
     static constexpr uint32_t B_SBO = 8 * B_ROW;
     static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;
-    // TMEM columns: unit u: D_hi [2 NH u, +NH), D_corr [2 NH u + NH, +NH); A stages
+    // TMEM columns: buffer u: D_hi [2 BN u, +BN), D_corr [2 BN u + BN, +BN); A stages
     // from A_COL0: per slot A_hi (ACOLS/2 columns) then A_lo
     static constexpr uint32_t ACOLS = MODE == 0 ? 32 : 64;     // 32 k of hi + lo
-    static constexpr uint32_t A_COL0 = NUNIT * 2 * NH;
+    static constexpr uint32_t A_COL0 = DBUF * 2 * BN;
     static constexpr uint32_t TMEM_COLS = 512;
-    // operand slots: as many A stages as TMEM holds (column halves keep a k-block's
-    // slots resident across both halves, so they need more slots to run ahead)
-    static constexpr int SOP_MAX = HALVES == 2 ? 8 : 4;
-    static constexpr int SOP = (TMEM_COLS - A_COL0) / ACOLS < SOP_MAX ? (TMEM_COLS - A_COL0) / ACOLS : SOP_MAX;
+    static constexpr int ASLOTS = (TMEM_COLS - A_COL0) / ACOLS;   // A stages TMEM holds
+    // operand ring: B_hi/B_lo in shared memory (and the A stage in TMEM unless ASTAT)
+    static constexpr int SOP = ASLOTS < 4 ? ASLOTS : 4;
     // FP32 stages: as many as fit next to the operand ring and C staging (<= 5)
-    static constexpr int S32_FIT = (232448 - 2048 - SOP * 2 * (BNC * 32 * (MODE == 0 ? 2 : 4)) - BM * BN * 4) /
-                                   (32 * BM * 4 + 32 * BNC * 4);
+    static constexpr int S32_FIT = (232448 - 2048 - SOP * OP_STAGE - CSTAGE_BYTES) / F32_STAGE;
     static constexpr int S32 = S32_FIT < 5 ? S32_FIT : 5;
-    static constexpr uint32_t KCOLS = MODE == 0 ? 8 : 8;       // TMEM columns per MMA K step
+    static constexpr uint32_t KCOLS = 8;                       // TMEM columns per MMA K step
     static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
-    static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4) + 16;
+    static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4 + ASLOTS) + 16;
     static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + CSTAGE_BYTES + BAR_BYTES;
     // warpgroup 0: producer, MMA issuer, 2 idle; warpgroups 1-2: 8 splitter warps
     // (2 per TMEM lane quadrant, 16 k each); warpgroups 3-6: 16 combine warps (4 per
-    // lane quadrant, 32 accumulator columns each -- a short drain matters here
-    // because the single accumulator buffer makes the MMA wait for it)
+    // lane quadrant, BN/4 accumulator columns each -- a short drain matters because
+    // the MMA waits for it)
     static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 8;
     static constexpr int EPI_WARP0 = 12, NUM_EPI_WARPS = 16;
     static constexpr int B_THREADS = BNC * 4;                // splitter threads with B work (2 chunks each)
@@ -78,10 +82,7 @@ struct PairTsCfg {
     static constexpr int NUM_THREADS = 32 * (EPI_WARP0 + NUM_EPI_WARPS);
     static constexpr int KS = BK / (NUM_SPLIT_WARPS / 4);   // k per splitter warp (A)
     static constexpr int ECOLS = BN / (NUM_EPI_WARPS / 4);  // accumulator columns per combine warp
-    // single buffer: the correction products and P1 get their own full/empty barriers, so
-    // the drain of D_corr overlaps P1 and the drain of D_hi overlaps the next k-block's
-    // correction products (no extra TMEM; the combine holds one part in registers)
-    static constexpr bool SPLITC = SPLITC_ && DBUF == 1 && HALVES == 1;
+    // SPLITC: the combine holds one part (D_corr) in registers while P1 runs
     static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = SPLITC ? 56 : 64, REGS_EPI = SPLITC ? 88 : 80;
     static_assert(128 * REGS_CTRL + 32 * NUM_SPLIT_WARPS * REGS_SPLIT + 32 * NUM_EPI_WARPS * REGS_EPI <= 65536,
                   "register budget");
@@ -90,12 +91,27 @@ struct PairTsCfg {
     static_assert(ECOLS % 8 == 0, "combine columns");
 };
 
-template <int MODE, bool RANGE, int BN, int HALVES, bool SPLITC_>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, HALVES, SPLITC_>::NUM_THREADS, 1)
+// tile j of work unit u: A-stationary -> n-tile j of (batch, m-pair) row block u;
+// otherwise unit u is tile u of the grouped raster
+template <bool ASTAT>
+__device__ __forceinline__ void ts_unit_tile(const GemmParams& p, long long u, int j, int& b, int& mt, int& nt)
+{
+    if (ASTAT) {
+        b = (int)(u / p.tiles_m);
+        mt = (int)(u - (long long)b * p.tiles_m);
+        nt = j;
+    } else {
+        tile_coords(p, u, b, mt, nt);
+    }
+}
+
+template <int MODE, bool RANGE, int BN, bool SPLITC_, bool ASTAT_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, SPLITC_, ASTAT_>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
 {
-    using Cfg = PairTsCfg<MODE, BN, HALVES, SPLITC_>;
+    using Cfg = PairTsCfg<MODE, BN, SPLITC_, ASTAT_>;
+    constexpr bool ASTAT = Cfg::ASTAT;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* f32buf = smem;
@@ -106,14 +122,17 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     uint64_t* f32_empty = f32_full + Cfg::S32;
     uint64_t* op_full = f32_empty + Cfg::S32;
     uint64_t* op_empty = op_full + Cfg::SOP;
-    uint64_t* acc_full = op_empty + Cfg::SOP;   // [DBUF]
-    uint64_t* acc_empty = acc_full + 2;         // [DBUF]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* acc_full = op_empty + Cfg::SOP;   // [DBUF] (SPLITC: [0] D_hi, [1] D_corr)
+    uint64_t* acc_empty = acc_full + 2;
+    uint64_t* aslot_empty = acc_empty + 2;      // [ASLOTS] (ASTAT)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aslot_empty + Cfg::ASLOTS);
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     const uint32_t rank = ptx::cluster_ctarank();
     const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const long long num_units = p.num_units;
+    const int R = ASTAT ? p.unit_tiles : 1;
     PROF_DECL
 #ifdef EMU_PROF
     const long long prof_start = clock64();
@@ -130,8 +149,9 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&acc_full[i], 1);
-            ptx::mbar_init(&acc_empty[i], 2 * Cfg::NUM_EPI_WARPS / Cfg::HALVES);
+            ptx::mbar_init(&acc_empty[i], 2 * Cfg::NUM_EPI_WARPS);
         }
+        for (int i = 0; i < Cfg::ASLOTS; ++i) ptx::mbar_init(&aslot_empty[i], 1);
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
@@ -151,41 +171,118 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             // -------------------------------------------- TMA producer (both CTAs)
             if (ptx::elect_one()) {
                 uint32_t s = 0, ph = 0;
-                for (long long t = cid; t < p.num_tiles; t += ncl) {
-                    int b, mt, nt;
-                    tile_coords(p, t, b, mt, nt);
-                    const int ab = p.a_batched ? b : 0, bb = p.b_batched ? b : 0;
-                    for (int ks = 0; ks < nks; ++ks) {
-                        PROF_T0();
-                        ptx::mbar_wait_sleep(&f32_empty[s], ph ^ 1);
-                        PROF_ADD(P_PROD_WAIT_EMPTY);
-                        uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
-                        ptx::mbar_arrive_expect_tx(&f32_full[s], Cfg::F32_STAGE);
-                        ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab);
-#pragma unroll
-                        for (int h = 0; h < Cfg::HALVES; ++h)   // CTA r: columns [NH h + NH/2 r, +NH/2) of each half
-                            ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES + h * (Cfg::BNC / Cfg::HALVES) * 128, &tmB,
-                                                    &f32_full[s], ks * Cfg::BK,
-                                                    nt * Cfg::BN + h * Cfg::NH + rank * (Cfg::NH / 2), bb);
-                        if (++s == Cfg::S32) { s = 0; ph ^= 1; }
+                for (long long u = cid; u < num_units; u += ncl) {
+                    for (int j = 0; j < R; ++j) {
+                        int b, mt, nt;
+                        ts_unit_tile<ASTAT>(p, u, j, b, mt, nt);
+                        const int ab = p.a_batched ? b : 0, bb = p.b_batched ? b : 0;
+                        const bool loadA = !ASTAT || j == 0;
+                        for (int ks = 0; ks < nks; ++ks) {
+                            PROF_T0();
+                            ptx::mbar_wait_sleep(&f32_empty[s], ph ^ 1);
+                            PROF_ADD(P_PROD_WAIT_EMPTY);
+                            uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
+                            ptx::mbar_arrive_expect_tx(&f32_full[s], loadA ? Cfg::F32_STAGE : Cfg::B32_BYTES);
+                            if (loadA)
+                                ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM,
+                                                        ks * Cfg::BK, ab);
+                            ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
+                                                    nt * Cfg::BN + rank * Cfg::BNC, bb);
+                            if (++s == Cfg::S32) { s = 0; ph ^= 1; }
+                        }
                     }
                 }
             }
         } else if (warp == 1) {
             // -------------------------------------------- MMA issuer (leader CTA only)
             if (rank == 0 && ptx::elect_one()) {
-                constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 0u, 0u, 256, Cfg::NH);
+                constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 0u, 0u, 256, Cfg::BN);
                 uint32_t s0 = 0, ph0 = 0, acc_it = 0;
                 if constexpr (Cfg::SPLITC) {
                     // per k-block: P2 + P3 into D_corr (barrier pair 1), then P1 into D_hi (pair 0)
-                    for (long long t = cid; t < p.num_tiles; t += ncl) {
+                    const uint32_t d_hi = tmem_base, d_corr = tmem_base + Cfg::BN;
+                    for (long long u = cid; u < num_units; u += ncl) {
+                        for (int j = 0; j < R; ++j) {
+                            const bool lastA = ASTAT && j == R - 1;   // release the A slots after this tile
+                            for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                                const int ks0 = kb * p.kb_stages;
+                                const int ks1 = min(ks0 + p.kb_stages, nks);
+                                const uint32_t aph = acc_it & 1u;
+                                PROF_T0();
+                                ptx::mbar_wait(&acc_empty[1], aph ^ 1u);
+                                PROF_ADD(P_MMA_WAIT_ACC);
+                                ptx::tc_fence_after();
+                                uint32_t s = s0, ph = ph0;
+                                for (int ks = ks0; ks < ks1; ++ks) {
+                                    PROF_T0();
+                                    ptx::mbar_wait(&op_full[s], ph);
+                                    PROF_ADD(P_MMA_WAIT_OP);
+                                    ptx::tc_fence_after();
+                                    PROF_T0();
+                                    if (p.corr) {
+                                        const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
+                                        const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                                        const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                                        for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                            const uint64_t dB_hi =
+                                                ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                            const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
+                                                                                  Cfg::B_SBO, Cfg::B_LAYOUT);
+                                            const uint32_t ka = st * Cfg::KCOLS;
+                                            const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                            if (MODE == 0) {
+                                                ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);   // P2
+                                                ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);    // P3
+                                            } else {
+                                                ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
+                                                ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
+                                            }
+                                        }
+                                    }
+                                    PROF_ADD(P_MMA_ISSUE);
+                                    if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                                }
+                                ptx::tc_commit_pair(&acc_full[1], 0x3);
+                                PROF_T0();
+                                ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
+                                PROF_ADD(P_MMA_WAIT_ACC);
+                                ptx::tc_fence_after();
+                                PROF_T0();
+                                s = s0; ph = ph0;
+                                for (int ks = ks0; ks < ks1; ++ks) {
+                                    const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
+                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                                    for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                        const uint64_t dB_hi =
+                                            ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                        if (MODE == 0)
+                                            ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
+                                        else
+                                            ptx::mma_tf32_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);
+                                    }
+                                    ptx::tc_commit_pair(&op_empty[s], 0x3);   // B (and non-stationary A) slot free
+                                    if (lastA) ptx::tc_commit_pair(&aslot_empty[ks], 0x3);
+                                    if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                                }
+                                ptx::tc_commit_pair(&acc_full[0], 0x3);
+                                PROF_ADD(P_MMA_ISSUE);
+                                s0 = s; ph0 = ph;
+                            }
+                        }
+                    }
+                } else {
+                    for (long long u = cid; u < num_units; u += ncl) {
                         for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                             const int ks0 = kb * p.kb_stages;
                             const int ks1 = min(ks0 + p.kb_stages, nks);
-                            const uint32_t aph = acc_it & 1u;
-                            const uint32_t d_hi = tmem_base, d_corr = tmem_base + Cfg::NH;
+                            const uint32_t buf = Cfg::DBUF == 2 ? (acc_it & 1u) : 0u;
+                            const uint32_t aph = (Cfg::DBUF == 2) ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
+                            const uint32_t d_hi = tmem_base + buf * 2 * Cfg::BN, d_corr = d_hi + Cfg::BN;
                             PROF_T0();
-                            ptx::mbar_wait(&acc_empty[1], aph ^ 1u);
+                            ptx::mbar_wait(&acc_empty[buf], aph ^ 1u);
                             PROF_ADD(P_MMA_WAIT_ACC);
                             ptx::tc_fence_after();
                             uint32_t s = s0, ph = ph0;
@@ -195,86 +292,9 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 PROF_ADD(P_MMA_WAIT_OP);
                                 ptx::tc_fence_after();
                                 PROF_T0();
-                                if (p.corr) {
-                                    const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
-                                    const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
-                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
-#pragma unroll
-                                    for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                        const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                        const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
-                                                                              Cfg::B_SBO, Cfg::B_LAYOUT);
-                                        const uint32_t ka = st * Cfg::KCOLS;
-                                        const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
-                                        if (MODE == 0) {
-                                            ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);   // P2
-                                            ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);    // P3
-                                        } else {
-                                            ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
-                                            ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
-                                        }
-                                    }
-                                }
-                                PROF_ADD(P_MMA_ISSUE);
-                                if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
-                            }
-                            ptx::tc_commit_pair(&acc_full[1], 0x3);
-                            PROF_T0();
-                            ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
-                            PROF_ADD(P_MMA_WAIT_ACC);
-                            ptx::tc_fence_after();
-                            PROF_T0();
-                            s = s0; ph = ph0;
-                            for (int ks = ks0; ks < ks1; ++ks) {
-                                const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
-                                const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
-#pragma unroll
-                                for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                    const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                    const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
-                                    if (MODE == 0) ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
-                                    else ptx::mma_tf32_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);
-                                }
-                                ptx::tc_commit_pair(&op_empty[s], 0x3);   // slot free
-                                if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
-                            }
-                            ptx::tc_commit_pair(&acc_full[0], 0x3);
-                            PROF_ADD(P_MMA_ISSUE);
-                            s0 = s; ph0 = ph;
-                        }
-                    }
-                } else
-                for (long long t = cid; t < p.num_tiles; t += ncl) {
-                    for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
-                        const int ks0 = kb * p.kb_stages;
-                        const int ks1 = min(ks0 + p.kb_stages, nks);
-                        uint32_t s = s0, ph = ph0;
-                        // HALVES == 2: all MMAs of column half 0 for the k-block, commit its
-                        // accumulator, then half 1 -- the drain of half 0 overlaps half 1's MMAs.
-                        // The k-block's operand slots stay resident until half 1 is issued.
-#pragma unroll 1
-                        for (int h = 0; h < Cfg::HALVES; ++h) {
-                            const uint32_t unit = Cfg::HALVES == 2 ? (uint32_t)h
-                                                : (Cfg::DBUF == 2 ? (acc_it & 1u) : 0u);
-                            const uint32_t aph = (Cfg::DBUF == 2) ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
-                            const uint32_t d_hi = tmem_base + unit * 2 * Cfg::NH, d_corr = d_hi + Cfg::NH;
-                            PROF_T0();
-                            ptx::mbar_wait(&acc_empty[unit], aph ^ 1u);
-                            PROF_ADD(P_MMA_WAIT_ACC);
-                            ptx::tc_fence_after();
-                            s = s0; ph = ph0;
-                            for (int ks = ks0; ks < ks1; ++ks) {
-                                if (h == 0) {
-                                    PROF_T0();
-                                    ptx::mbar_wait(&op_full[s], ph);
-                                    PROF_ADD(P_MMA_WAIT_OP);
-                                    ptx::tc_fence_after();
-                                }
-                                PROF_T0();
                                 const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
                                 const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
-                                const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE) +
-                                                       h * (Cfg::BNC / Cfg::HALVES) * Cfg::B_ROW;
+                                const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
 #pragma unroll
                                 for (int st = 0; st < Cfg::NSTEPS; ++st) {
                                     const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
@@ -296,13 +316,13 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                         }
                                     }
                                 }
-                                if (h == Cfg::HALVES - 1) ptx::tc_commit_pair(&op_empty[s], 0x3);   // slot free
+                                ptx::tc_commit_pair(&op_empty[s], 0x3);   // slot free
                                 PROF_ADD(P_MMA_ISSUE);
                                 if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                             }
-                            ptx::tc_commit_pair(&acc_full[unit], 0x3);
+                            ptx::tc_commit_pair(&acc_full[buf], 0x3);
+                            s0 = s; ph0 = ph;
                         }
-                        s0 = s; ph0 = ph;
                     }
                 }
             }
@@ -317,93 +337,101 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t n = tid % Cfg::BNC, quarter = tid / Cfg::BNC;  // B: 8 k per thread (tid < B_THREADS)
         const bool has_b = tid < Cfg::B_THREADS;
         const uint32_t tq = tmem_base + ((q * 32u) << 16);
-        uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0;
+        uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0, unit_it = 0;
         uint32_t nonfinite = 0;
-        for (long long t = cid; t < p.num_tiles; t += ncl) {
-            for (int ks = 0; ks < nks; ++ks) {
-                PROF_T0();
-                ptx::mbar_wait(&f32_full[s32], ph32);
-                PROF_ADD(P_SPL_WAIT_F32);
-                PROF_T0();
-                ptx::mbar_wait(&op_empty[sop], phop ^ 1);
-                PROF_ADD(P_SPL_WAIT_OP);
-                PROF_T0();
-                ptx::tc_fence_after();
-                const float* fa = reinterpret_cast<const float*>(f32buf + s32 * Cfg::F32_STAGE);
-                const uint8_t* fb = f32buf + s32 * Cfg::F32_STAGE + Cfg::A32_BYTES;
-                uint8_t* ob_hi = opbuf + sop * Cfg::OP_STAGE;
-                uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
-                // ---- load phase: A(m, KS kq .. +KS-1) (a warp reads 32 consecutive m per k),
-                //      B(8 quarter .. +7, n): FP32 16-byte chunks 2 quarter, 2 quarter + 1 of row n
-                float av[Cfg::KS];
+        for (long long u = cid; u < num_units; u += ncl, ++unit_it) {
+            for (int j = 0; j < R; ++j) {
+                const bool doA = !ASTAT || j == 0;
+                for (int ks = 0; ks < nks; ++ks) {
+                    PROF_T0();
+                    ptx::mbar_wait(&f32_full[s32], ph32);
+                    PROF_ADD(P_SPL_WAIT_F32);
+                    PROF_T0();
+                    ptx::mbar_wait(&op_empty[sop], phop ^ 1);
+                    if (ASTAT && j == 0) ptx::mbar_wait(&aslot_empty[ks], (unit_it & 1u) ^ 1u);
+                    PROF_ADD(P_SPL_WAIT_OP);
+                    PROF_T0();
+                    ptx::tc_fence_after();
+                    const float* fa = reinterpret_cast<const float*>(f32buf + s32 * Cfg::F32_STAGE);
+                    const uint8_t* fb = f32buf + s32 * Cfg::F32_STAGE + Cfg::A32_BYTES;
+                    uint8_t* ob_hi = opbuf + sop * Cfg::OP_STAGE;
+                    uint8_t* ob_lo = ob_hi + Cfg::BOP_BYTES;
+                    // ---- load phase: A(m, KS kq .. +KS-1) (a warp reads 32 consecutive m per k),
+                    //      B(8 quarter .. +7, n): FP32 16-byte chunks 2 quarter, 2 quarter + 1 of row n
+                    float av[Cfg::KS];
+                    if (doA) {
 #pragma unroll
-                for (int j = 0; j < Cfg::KS; ++j) av[j] = fa[(kq * Cfg::KS + j) * Cfg::BM + m];
-                float4 vb[2];
-                if (has_b) {
-#pragma unroll
-                    for (int c = 0; c < 2; ++c)
-                        vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
-                }
-                // ---- A: split into TMEM columns (lane = m)
-                const uint32_t a_hi = tq + Cfg::A_COL0 + sop * Cfg::ACOLS;
-                const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
-                if (MODE == 0) {
-                    uint32_t h[Cfg::KS / 2], l[Cfg::KS / 2];
-#pragma unroll
-                    for (int j = 0; j < Cfg::KS / 2; ++j) {
-                        split_fp16x2(av[2 * j], av[2 * j + 1], h[j], l[j]);
-                        if (RANGE) nonfinite |= f16x2_nonfinite(h[j]);
+                        for (int jj = 0; jj < Cfg::KS; ++jj) av[jj] = fa[(kq * Cfg::KS + jj) * Cfg::BM + m];
                     }
-                    ptx::tmem_st8(a_hi + kq * (Cfg::KS / 2), h);
-                    ptx::tmem_st8(a_lo + kq * (Cfg::KS / 2), l);
-                } else {
+                    float4 vb[2];
+                    if (has_b) {
 #pragma unroll
-                    for (int c = 0; c < Cfg::KS / 8; ++c) {
-                        uint32_t h[8], l[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) split_tf32(av[8 * c + j], h[j], l[j]);
-                        ptx::tmem_st8(a_hi + kq * Cfg::KS + 8 * c, h);
-                        ptx::tmem_st8(a_lo + kq * Cfg::KS + 8 * c, l);
+                        for (int c = 0; c < 2; ++c)
+                            vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
                     }
-                }
-                // ---- B: split into the K-major operand tile in shared memory
-                if (!has_b) {
-                } else if (MODE == 0) {
-                    // one 16-byte FP16 chunk (8 k), K-major SWIZZLE_64B rows
-                    uint2 h0, l0, h1, l1;
-                    split4_fp16(vb[0], h0, l0);
-                    split4_fp16(vb[1], h1, l1);
-                    if (RANGE)
-                        nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) | f16x2_nonfinite(h1.x) |
-                                     f16x2_nonfinite(h1.y);
-                    const uint32_t off = n * 64 + ((quarter ^ ((n >> 1) & 3)) << 4);
-                    *reinterpret_cast<uint4*>(ob_hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
-                    *reinterpret_cast<uint4*>(ob_lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
-                } else {
+                    // ---- A: split into TMEM columns (lane = m)
+                    if (doA) {
+                        const uint32_t a_hi = tq + Cfg::A_COL0 + (ASTAT ? (uint32_t)ks : sop) * Cfg::ACOLS;
+                        const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                        if (MODE == 0) {
+                            uint32_t h[Cfg::KS / 2], l[Cfg::KS / 2];
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {   // two 16-byte TF32 chunks, K-major SWIZZLE_128B rows
-                        const uint32_t j = 2 * quarter + c;
-                        uint4 h, l;
-                        split_tf32(vb[c].x, h.x, l.x);
-                        split_tf32(vb[c].y, h.y, l.y);
-                        split_tf32(vb[c].z, h.z, l.z);
-                        split_tf32(vb[c].w, h.w, l.w);
-                        const uint32_t off = n * 128 + ((j ^ (n & 7)) << 4);
-                        *reinterpret_cast<uint4*>(ob_hi + off) = h;
-                        *reinterpret_cast<uint4*>(ob_lo + off) = l;
+                            for (int jj = 0; jj < Cfg::KS / 2; ++jj) {
+                                split_fp16x2(av[2 * jj], av[2 * jj + 1], h[jj], l[jj]);
+                                if (RANGE) nonfinite |= f16x2_nonfinite(h[jj]);
+                            }
+                            ptx::tmem_st8(a_hi + kq * (Cfg::KS / 2), h);
+                            ptx::tmem_st8(a_lo + kq * (Cfg::KS / 2), l);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < Cfg::KS / 8; ++c) {
+                                uint32_t h[8], l[8];
+#pragma unroll
+                                for (int jj = 0; jj < 8; ++jj) split_tf32(av[8 * c + jj], h[jj], l[jj]);
+                                ptx::tmem_st8(a_hi + kq * Cfg::KS + 8 * c, h);
+                                ptx::tmem_st8(a_lo + kq * Cfg::KS + 8 * c, l);
+                            }
+                        }
                     }
+                    // ---- B: split into the K-major operand tile in shared memory
+                    if (!has_b) {
+                    } else if (MODE == 0) {
+                        // one 16-byte FP16 chunk (8 k), K-major SWIZZLE_64B rows
+                        uint2 h0, l0, h1, l1;
+                        split4_fp16(vb[0], h0, l0);
+                        split4_fp16(vb[1], h1, l1);
+                        if (RANGE)
+                            nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) | f16x2_nonfinite(h1.x) |
+                                         f16x2_nonfinite(h1.y);
+                        const uint32_t off = n * 64 + ((quarter ^ ((n >> 1) & 3)) << 4);
+                        *reinterpret_cast<uint4*>(ob_hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+                        *reinterpret_cast<uint4*>(ob_lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {   // two 16-byte TF32 chunks, K-major SWIZZLE_128B rows
+                            const uint32_t jj = 2 * quarter + c;
+                            uint4 h, l;
+                            split_tf32(vb[c].x, h.x, l.x);
+                            split_tf32(vb[c].y, h.y, l.y);
+                            split_tf32(vb[c].z, h.z, l.z);
+                            split_tf32(vb[c].w, h.w, l.w);
+                            const uint32_t off = n * 128 + ((jj ^ (n & 7)) << 4);
+                            *reinterpret_cast<uint4*>(ob_hi + off) = h;
+                            *reinterpret_cast<uint4*>(ob_lo + off) = l;
+                        }
+                    }
+                    ptx::fence_proxy_async_smem();   // B tiles -> async proxy
+                    if (doA) ptx::tmem_wait_st();    // A columns written
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    PROF_ADD(P_SPL_WORK);
+                    if (lane == 0) {
+                        ptx::mbar_arrive_cluster(ptx::mapa_shared(&op_full[sop], 0));
+                        ptx::mbar_arrive(&f32_empty[s32]);
+                    }
+                    if (++s32 == Cfg::S32) { s32 = 0; ph32 ^= 1; }
+                    if (++sop == Cfg::SOP) { sop = 0; phop ^= 1; }
                 }
-                ptx::fence_proxy_async_smem();   // B tiles -> async proxy
-                ptx::tmem_wait_st();             // A columns written
-                ptx::tc_fence_before();
-                __syncwarp();
-                PROF_ADD(P_SPL_WORK);
-                if (lane == 0) {
-                    ptx::mbar_arrive_cluster(ptx::mapa_shared(&op_full[sop], 0));
-                    ptx::mbar_arrive(&f32_empty[s32]);
-                }
-                if (++s32 == Cfg::S32) { s32 = 0; ph32 ^= 1; }
-                if (++sop == Cfg::SOP) { sop = 0; phop ^= 1; }
             }
         }
         if (RANGE) {
@@ -417,149 +445,150 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t e = warp - Cfg::EPI_WARP0;
         const uint32_t q = warp & 3;
         const uint32_t h = e >> 2;                     // column group: tile columns [HALF h, +HALF)
-        // accumulator unit holding those columns (HALVES == 2: the column half)
-        const uint32_t my_half = Cfg::HALVES == 2 ? (h * HALF) / Cfg::NH : 0u;
-        const uint32_t col_in_unit = h * HALF - my_half * Cfg::NH;
         const float scale = MODE == 0 ? (1.0f / 2048.0f) : 1.0f;
         const uint32_t acc_empty_leader = ptx::mapa_shared(&acc_empty[0], 0);   // + 8 * buffer
         uint32_t acc_it = 0;
-        for (long long t = cid; t < p.num_tiles; t += ncl) {
-            int b, mt, nt;
-            tile_coords(p, t, b, mt, nt);
-            float creg[HALF];
+        for (long long u = cid; u < num_units; u += ncl) {
+            for (int j = 0; j < R; ++j) {
+                int b, mt, nt;
+                ts_unit_tile<ASTAT>(p, u, j, b, mt, nt);
+                float creg[HALF];
 #pragma unroll
-            for (int j = 0; j < HALF; ++j) creg[j] = 0.0f;
-            if constexpr (Cfg::SPLITC) {
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + h * HALF;
-                const uint32_t emp_hi = ptx::mapa_shared(&acc_empty[0], 0), emp_corr = emp_hi + 8;
-                for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
-                    const uint32_t aph = acc_it & 1u;
-                    // D_corr first (P2 + P3 are issued first); hold it while P1 runs
-                    PROF_T0();
-                    ptx::mbar_wait(&acc_full[1], aph);
-                    PROF_ADD(P_EPI_WAIT_ACC);
-                    PROF_T0();
-                    ptx::tc_fence_after();
-                    float vc[HALF / 8][8];
-                    if (p.corr) {
-#pragma unroll
-                        for (int c = 0; c < HALF / 8; ++c) ptx::tmem_ld8(taddr + Cfg::NH + c * 8, vc[c]);
-                        ptx::tmem_wait_ld();
-                    }
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(emp_corr);
-                    PROF_ADD(P_EPI_DRAIN);
-                    PROF_T0();
-                    ptx::mbar_wait(&acc_full[0], aph);
-                    PROF_ADD(P_EPI_WAIT_ACC);
-                    PROF_T0();
-                    ptx::tc_fence_after();
-                    constexpr int CPW = 2;
-#pragma unroll
-                    for (int c0 = 0; c0 < HALF / 8; c0 += CPW) {
-                        float vh[CPW][8];
-#pragma unroll
-                        for (int c = 0; c < CPW; ++c) ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
-                        ptx::tmem_wait_ld();
-                        if (c0 + CPW >= HALF / 8) {   // last chunk read: release D_hi before the math
-                            ptx::tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) ptx::mbar_arrive_cluster(emp_hi);
-                        }
-#pragma unroll
-                        for (int c = 0; c < CPW; ++c) {
-                            float* cr = creg + (c0 + c) * 8;
-                            const float* cc = vc[c0 + c];
-                            if (p.corr) {
-#pragma unroll
-                                for (int j = 0; j < 8; j += 2)
-                                    combine2(cr[j], cr[j + 1], vh[c][j], vh[c][j + 1], cc[j], cc[j + 1], scale);
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) cr[j] = __fadd_rn(cr[j], vh[c][j]);
-                            }
-                        }
-                    }
-                    PROF_ADD(P_EPI_DRAIN);
-                }
-            } else
-            for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
-                const uint32_t buf = Cfg::HALVES == 2 ? my_half : (Cfg::DBUF == 2 ? (acc_it & 1u) : 0u);
-                const uint32_t aph = Cfg::DBUF == 2 ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
-                PROF_T0();
-                ptx::mbar_wait(&acc_full[buf], aph);   // on the critical path: spin, do not sleep
-                PROF_ADD(P_EPI_WAIT_ACC);
-                PROF_T0();
-                ptx::tc_fence_after();
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * Cfg::NH + col_in_unit;
-                // columns in chunks of 8; CPW chunks loaded per tcgen05.wait::ld
-                constexpr int NCH = HALF / 8, CPW = (HALF <= 24) ? NCH : 2;
-#pragma unroll
-                for (int c0 = 0; c0 < NCH; c0 += CPW) {
-                    float vh[CPW][8], vc[CPW][8];
-#pragma unroll
-                    for (int c = 0; c < CPW; ++c) {
-                        ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
-                        ptx::tmem_ld8(taddr + Cfg::NH + (c0 + c) * 8, vc[c]);
-                    }
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < CPW; ++c) {
-                        float* cr = creg + (c0 + c) * 8;
+                for (int jj = 0; jj < HALF; ++jj) creg[jj] = 0.0f;
+                if constexpr (Cfg::SPLITC) {
+                    const uint32_t taddr = tmem_base + ((q * 32u) << 16) + h * HALF;
+                    const uint32_t emp_hi = acc_empty_leader, emp_corr = acc_empty_leader + 8;
+                    for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                        const uint32_t aph = acc_it & 1u;
+                        // D_corr first (P2 + P3 are issued first); hold it while P1 runs
+                        PROF_T0();
+                        ptx::mbar_wait(&acc_full[1], aph);
+                        PROF_ADD(P_EPI_WAIT_ACC);
+                        PROF_T0();
+                        ptx::tc_fence_after();
+                        float vc[HALF / 8][8];
                         if (p.corr) {
 #pragma unroll
-                            for (int j = 0; j < 8; j += 2)
-                                combine2(cr[j], cr[j + 1], vh[c][j], vh[c][j + 1], vc[c][j], vc[c][j + 1], scale);
+                            for (int c = 0; c < HALF / 8; ++c) ptx::tmem_ld8(taddr + Cfg::BN + c * 8, vc[c]);
+                            ptx::tmem_wait_ld();
+                        }
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive_cluster(emp_corr);
+                        PROF_ADD(P_EPI_DRAIN);
+                        PROF_T0();
+                        ptx::mbar_wait(&acc_full[0], aph);
+                        PROF_ADD(P_EPI_WAIT_ACC);
+                        PROF_T0();
+                        ptx::tc_fence_after();
+                        constexpr int CPW = 2;
+#pragma unroll
+                        for (int c0 = 0; c0 < HALF / 8; c0 += CPW) {
+                            float vh[CPW][8];
+#pragma unroll
+                            for (int c = 0; c < CPW; ++c) ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
+                            ptx::tmem_wait_ld();
+                            if (c0 + CPW >= HALF / 8) {   // last chunk read: release D_hi before the math
+                                ptx::tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) ptx::mbar_arrive_cluster(emp_hi);
+                            }
+#pragma unroll
+                            for (int c = 0; c < CPW; ++c) {
+                                float* cr = creg + (c0 + c) * 8;
+                                const float* cc = vc[c0 + c];
+                                if (p.corr) {
+#pragma unroll
+                                    for (int jj = 0; jj < 8; jj += 2)
+                                        combine2(cr[jj], cr[jj + 1], vh[c][jj], vh[c][jj + 1], cc[jj], cc[jj + 1], scale);
+                                } else {
+#pragma unroll
+                                    for (int jj = 0; jj < 8; ++jj) cr[jj] = __fadd_rn(cr[jj], vh[c][jj]);
+                                }
+                            }
+                        }
+                        PROF_ADD(P_EPI_DRAIN);
+                    }
+                } else {
+                    for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
+                        const uint32_t buf = Cfg::DBUF == 2 ? (acc_it & 1u) : 0u;
+                        const uint32_t aph = Cfg::DBUF == 2 ? ((acc_it >> 1) & 1u) : (acc_it & 1u);
+                        PROF_T0();
+                        ptx::mbar_wait(&acc_full[buf], aph);   // on the critical path: spin, do not sleep
+                        PROF_ADD(P_EPI_WAIT_ACC);
+                        PROF_T0();
+                        ptx::tc_fence_after();
+                        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * Cfg::BN + h * HALF;
+                        // columns in chunks of 8; CPW chunks loaded per tcgen05.wait::ld
+                        constexpr int NCH = HALF / 8, CPW = (HALF <= 24) ? NCH : 2;
+#pragma unroll
+                        for (int c0 = 0; c0 < NCH; c0 += CPW) {
+                            float vh[CPW][8], vc[CPW][8];
+#pragma unroll
+                            for (int c = 0; c < CPW; ++c) {
+                                ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
+                                ptx::tmem_ld8(taddr + Cfg::BN + (c0 + c) * 8, vc[c]);
+                            }
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int c = 0; c < CPW; ++c) {
+                                float* cr = creg + (c0 + c) * 8;
+                                if (p.corr) {
+#pragma unroll
+                                    for (int jj = 0; jj < 8; jj += 2)
+                                        combine2(cr[jj], cr[jj + 1], vh[c][jj], vh[c][jj + 1], vc[c][jj], vc[c][jj + 1],
+                                                 scale);
+                                } else {
+#pragma unroll
+                                    for (int jj = 0; jj < 8; ++jj) cr[jj] = __fadd_rn(cr[jj], vh[c][jj]);
+                                }
+                            }
+                        }
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader + 8 * buf);
+                        PROF_ADD(P_EPI_DRAIN);
+                    }
+                }
+                PROF_T0();
+                const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
+                if (p.tma_store) {
+                    const bool leader = (e == 0 && lane == 0);
+                    const uint32_t r = q * 32 + lane;
+                    if (leader) ptx::bulk_wait_group_read0();
+                    ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                    float* dst = cstage + h * HALF * Cfg::BM;
+#pragma unroll
+                    for (int jj = 0; jj < HALF; ++jj) dst[jj * Cfg::BM + r] = fmaf(p.alpha, creg[jj], 0.0f);
+                    ptx::fence_proxy_async_smem();
+                    ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
+                    if (leader) {
+#pragma unroll
+                        for (int c = 0; c < Cfg::BN / 32; ++c)
+                            ptx::tma_store_3d(&tmC, cstage + c * 32 * Cfg::BM, mrow0, nt * Cfg::BN + c * 32, b);
+                        ptx::bulk_commit_group();
+                    }
+                } else {
+                    const int r = mrow0 + (int)(q * 32 + lane);
+                    const int col0 = nt * Cfg::BN + (int)(h * HALF);
+                    if (r < p.m) {
+                        float* cp = p.C + (long long)b * p.strideC + r + (long long)col0 * p.ldc;
+                        if (p.beta != 0.0f) {
+#pragma unroll
+                            for (int jj = 0; jj < HALF; ++jj)
+                                if (col0 + jj < p.n) {
+                                    float* d = cp + (long long)jj * p.ldc;
+                                    *d = fmaf(p.alpha, creg[jj], __fmul_rn(p.beta, *d));
+                                }
                         } else {
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) cr[j] = __fadd_rn(cr[j], vh[c][j]);
+                            for (int jj = 0; jj < HALF; ++jj)
+                                if (col0 + jj < p.n) cp[(long long)jj * p.ldc] = fmaf(p.alpha, creg[jj], 0.0f);
                         }
                     }
                 }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_cluster(acc_empty_leader + 8 * buf);
-                PROF_ADD(P_EPI_DRAIN);
+                PROF_ADD(P_EPI_STORE);
             }
-            PROF_T0();
-            const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
-            if (p.tma_store) {
-                const bool leader = (e == 0 && lane == 0);
-                const uint32_t r = q * 32 + lane;
-                if (leader) ptx::bulk_wait_group_read0();
-                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
-                float* dst = cstage + h * HALF * Cfg::BM;
-#pragma unroll
-                for (int j = 0; j < HALF; ++j) dst[j * Cfg::BM + r] = fmaf(p.alpha, creg[j], 0.0f);
-                ptx::fence_proxy_async_smem();
-                ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
-                if (leader) {
-#pragma unroll
-                    for (int c = 0; c < Cfg::BN / 32; ++c)
-                        ptx::tma_store_3d(&tmC, cstage + c * 32 * Cfg::BM, mrow0, nt * Cfg::BN + c * 32, b);
-                    ptx::bulk_commit_group();
-                }
-            } else {
-                const int r = mrow0 + (int)(q * 32 + lane);
-                const int col0 = nt * Cfg::BN + (int)(h * HALF);
-                if (r < p.m) {
-                    float* cp = p.C + (long long)b * p.strideC + r + (long long)col0 * p.ldc;
-                    if (p.beta != 0.0f) {
-#pragma unroll
-                        for (int j = 0; j < HALF; ++j)
-                            if (col0 + j < p.n) {
-                                float* d = cp + (long long)j * p.ldc;
-                                *d = fmaf(p.alpha, creg[j], __fmul_rn(p.beta, *d));
-                            }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < HALF; ++j)
-                            if (col0 + j < p.n) cp[(long long)j * p.ldc] = fmaf(p.alpha, creg[j], 0.0f);
-                    }
-                }
-            }
-            PROF_ADD(P_EPI_STORE);
         }
         if (p.tma_store && warp == Cfg::EPI_WARP0 && lane == 0) ptx::bulk_wait_group0();
     }

@@ -159,6 +159,44 @@ def test_deterministic(mode):
     assert np.array_equal(C1, Ch)
 
 
+# --------------------------------------------------- A-stationary path ----
+# The TS kernel keeps the split A of a whole (item, 256-row) block in TMEM when
+# all of k fits its A slots (FP16 k <= 256, TF32 k <= 128), n spans >= 2 tiles of
+# 128 and there are >= 148 such row blocks (api.cu dispatch).  These shapes take
+# that path; with fewer row blocks the same problem takes the streaming-A path,
+# which issues the same MMAs in the same order, so the two agree bit for bit.
+ASTAT_SHAPES = [
+    (148, 256, 256, 128),    # two row blocks per cluster, full tiles
+    (150, 200, 300, 96),     # ragged m (one block), ragged n (3 tiles), 3 k-stages
+    (80, 512, 384, 64),      # 2 m-pairs x 80 = 160 row blocks, 3 n-tiles
+]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("shape", ASTAT_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_astat_parity(mode, shape):
+    batch, m, n, k = shape
+    A, B = workloads.make_operands(batch, m, n, k, seed=300 + n + k)
+    C, _ = _cmp(mode, A, B, m, n, k)
+    # the streaming-A path (too few row blocks for A-stationary) gives the same bits
+    half = batch // 2
+    Ch = np.concatenate([emu_gpu(mode, A[:half], B[:half], m, n, k),
+                         emu_gpu(mode, A[half:], B[half:], m, n, k)])
+    assert np.array_equal(C, Ch)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_astat_policies_and_epilogues(mode):
+    batch, m, n, k = 150, 200, 300, 96
+    A, B = workloads.make_operands(batch, m, n, k, seed=17)
+    _cmp(mode, A, B, m, n, k, kblock=32)
+    _cmp(mode, A, B, m, n, k, flags=1)
+    C0 = workloads.uniform((batch, n, m), seed=18)
+    _cmp(mode, A, B, m, n, k, alpha=0.5, beta=-2.0, C=C0)   # beta != 0: direct-store epilogue
+    Ai, Bi = workloads.make_operands(batch, m, n, k, seed=19, dist="int16")
+    assert np.array_equal(emu_gpu(mode, Ai, Bi, m, n, k), oracle.emu_gemm(mode, Ai, Bi, m, n, k))
+
+
 # -------------------------------------------------------- accuracy gates ----
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("k", [64, 256, 1024, 4096])

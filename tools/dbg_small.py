@@ -13,7 +13,7 @@ import workloads  # noqa: E402
 from gpu_util import emu_gpu, tolerance  # noqa: E402
 
 for mode in ("fp16", "tf32"):
-    for (batch, m, n, k) in [(1, 128, 128, 32), (1, 128, 128, 64), (1, 128, 128, 256), (2, 200, 136, 300), (1, 256, 128, 64), (3, 300, 260, 200),
+    for (batch, m, n, k) in [(150, 200, 300, 96), (1, 128, 128, 32), (1, 128, 128, 64), (1, 128, 128, 256), (2, 200, 136, 300), (1, 256, 128, 64), (3, 300, 260, 200),
                              (16, 64, 64, 64)]:
         A, B = workloads.make_operands(batch, m, n, k, seed=1)
         try:
