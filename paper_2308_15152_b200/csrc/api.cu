@@ -348,7 +348,8 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
                     (unsigned long long)strideC * 4 < (1ull << 40);
     if (tma_store) {
         const uint64_t sC = c_b ? (uint64_t)strideC : (((uint64_t)ldc * (uint64_t)n + 3) & ~uint64_t(3));
-        if (!make_map(&tmC, C, (uint64_t)m, (uint64_t)n, (uint64_t)ldc, c_b ? (uint64_t)batch : 1, sC, Cfg::BM, 32,
+        // one 32-row x ECOLS block per combine warp (each warp stores its own columns)
+        if (!make_map(&tmC, C, (uint64_t)m, (uint64_t)n, (uint64_t)ldc, c_b ? (uint64_t)batch : 1, sC, 32, Cfg::ECOLS,
                       CU_TENSOR_MAP_SWIZZLE_NONE))
             tma_store = 0;
     }
@@ -691,7 +692,19 @@ __attribute__((visibility("default"))) int emu_prof_read(unsigned long long* hos
 __attribute__((visibility("default"))) int emu_prof_reset(void)
 {
     unsigned long long z[16] = {};
+    unsigned int zc[emu::TRACE_ROLES] = {};
+    if (cudaMemcpyToSymbol(emu::g_trace_cnt, zc, sizeof(zc)) != cudaSuccess) return 1;
     return cudaMemcpyToSymbol(emu::g_prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+// trace of CTA 0 since the last reset: host receives TRACE_N (t, ev) pairs and the
+// per-role counts; returns the number of roles
+__attribute__((visibility("default"))) int emu_trace_read(long long* host, unsigned int* counts)
+{
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(counts, emu::g_trace_cnt, sizeof(unsigned int) * emu::TRACE_ROLES) != cudaSuccess)
+        return -1;
+    if (cudaMemcpyFromSymbol(host, emu::g_trace, sizeof(long long) * 2 * emu::TRACE_N) != cudaSuccess) return -1;
+    return emu::TRACE_ROLES;
 }
 #endif
 

@@ -62,8 +62,10 @@ struct PairTsCfg {
     static constexpr uint32_t A_COL0 = DBUF * 2 * BN;
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int ASLOTS = (TMEM_COLS - A_COL0) / ACOLS;   // A stages TMEM holds
-    // operand ring: B_hi/B_lo in shared memory (and the A stage in TMEM unless ASTAT)
-    static constexpr int SOP = ASLOTS < 4 ? ASLOTS : 4;
+    // operand ring: B_hi/B_lo in shared memory (and the A stage in TMEM unless ASTAT);
+    // FP16: 5 slots still leave room for 5 FP32 stages
+    static constexpr int SOP_MAX = MODE == 0 ? 5 : 4;
+    static constexpr int SOP = ASLOTS < SOP_MAX ? ASLOTS : SOP_MAX;
     // FP32 stages: as many as fit next to the operand ring and C staging (<= 5)
     static constexpr int S32_FIT = (232448 - 2048 - SOP * OP_STAGE - CSTAGE_BYTES) / F32_STAGE;
     static constexpr int S32 = S32_FIT < 5 ? S32_FIT : 5;
@@ -134,6 +136,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     const long long num_units = p.num_units;
     const int R = ASTAT ? p.unit_tiles : 1;
     PROF_DECL
+    TRACE_DECL
 #ifdef EMU_PROF
     const long long prof_start = clock64();
 #endif
@@ -182,6 +185,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                             ptx::mbar_wait_sleep(&f32_empty[s], ph ^ 1);
                             PROF_ADD(P_PROD_WAIT_EMPTY);
                             uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
+                            TRACE_AT(0, 1, ks);
                             ptx::mbar_arrive_expect_tx(&f32_full[s], loadA ? Cfg::F32_STAGE : Cfg::B32_BYTES);
                             if (loadA)
                                 ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM,
@@ -211,12 +215,14 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 PROF_T0();
                                 ptx::mbar_wait(&acc_empty[1], aph ^ 1u);
                                 PROF_ADD(P_MMA_WAIT_ACC);
+                                TRACE_AT(1, 5, kb);
                                 ptx::tc_fence_after();
                                 uint32_t s = s0, ph = ph0;
                                 for (int ks = ks0; ks < ks1; ++ks) {
                                     PROF_T0();
                                     ptx::mbar_wait(&op_full[s], ph);
                                     PROF_ADD(P_MMA_WAIT_OP);
+                                    TRACE_AT(1, 9, ks);
                                     ptx::tc_fence_after();
                                     PROF_T0();
                                     if (p.corr) {
@@ -244,9 +250,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                     if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                                 }
                                 ptx::tc_commit_pair(&acc_full[1], 0x3);
+                                TRACE_AT(1, 6, kb);
                                 PROF_T0();
                                 ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
                                 PROF_ADD(P_MMA_WAIT_ACC);
+                                TRACE_AT(1, 7, kb);
                                 ptx::tc_fence_after();
                                 PROF_T0();
                                 s = s0; ph = ph0;
@@ -269,6 +277,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 }
                                 ptx::tc_commit_pair(&acc_full[0], 0x3);
                                 PROF_ADD(P_MMA_ISSUE);
+                                TRACE_AT(1, 8, kb);
                                 s0 = s; ph0 = ph;
                             }
                         }
@@ -343,13 +352,17 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             for (int j = 0; j < R; ++j) {
                 const bool doA = !ASTAT || j == 0;
                 for (int ks = 0; ks < nks; ++ks) {
-                    PROF_T0();
-                    ptx::mbar_wait(&f32_full[s32], ph32);
-                    PROF_ADD(P_SPL_WAIT_F32);
+                    // operand slot first, then the FP32 stage: a stage is held only while it
+                    // is split, so the producer keeps the whole FP32 ring in flight
                     PROF_T0();
                     ptx::mbar_wait(&op_empty[sop], phop ^ 1);
                     if (ASTAT && j == 0) ptx::mbar_wait(&aslot_empty[ks], (unit_it & 1u) ^ 1u);
                     PROF_ADD(P_SPL_WAIT_OP);
+                    if (warp == Cfg::SPLIT_WARP0 && lane == 0) TRACE_AT(2, 3, ks);
+                    PROF_T0();
+                    ptx::mbar_wait(&f32_full[s32], ph32);
+                    PROF_ADD(P_SPL_WAIT_F32);
+                    if (warp == Cfg::SPLIT_WARP0 && lane == 0) TRACE_AT(2, 2, ks);
                     PROF_T0();
                     ptx::tc_fence_after();
                     const float* fa = reinterpret_cast<const float*>(f32buf + s32 * Cfg::F32_STAGE);
@@ -429,6 +442,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         ptx::mbar_arrive_cluster(ptx::mapa_shared(&op_full[sop], 0));
                         ptx::mbar_arrive(&f32_empty[s32]);
                     }
+                    if (warp == Cfg::SPLIT_WARP0 && lane == 0) TRACE_AT(2, 4, ks);
                     if (++s32 == Cfg::S32) { s32 = 0; ph32 ^= 1; }
                     if (++sop == Cfg::SOP) { sop = 0; phop ^= 1; }
                 }
@@ -464,6 +478,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         PROF_T0();
                         ptx::mbar_wait(&acc_full[1], aph);
                         PROF_ADD(P_EPI_WAIT_ACC);
+                        if (lane == 0) TRACE_AT(3 + e, 10, kb);
                         PROF_T0();
                         ptx::tc_fence_after();
                         float vc[HALF / 8][8];
@@ -476,9 +491,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive_cluster(emp_corr);
                         PROF_ADD(P_EPI_DRAIN);
+                        if (lane == 0) TRACE_AT(3 + e, 11, kb);
                         PROF_T0();
                         ptx::mbar_wait(&acc_full[0], aph);
                         PROF_ADD(P_EPI_WAIT_ACC);
+                        if (lane == 0) TRACE_AT(3 + e, 12, kb);
                         PROF_T0();
                         ptx::tc_fence_after();
                         constexpr int CPW = 2;
@@ -492,6 +509,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 ptx::tc_fence_before();
                                 __syncwarp();
                                 if (lane == 0) ptx::mbar_arrive_cluster(emp_hi);
+                                if (lane == 0) TRACE_AT(3 + e, 13, kb);
                             }
 #pragma unroll
                             for (int c = 0; c < CPW; ++c) {
@@ -551,21 +569,20 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     }
                 }
                 PROF_T0();
+                if (lane == 0) TRACE_AT(3 + e, 14, j);
                 const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
                 if (p.tma_store) {
-                    const bool leader = (e == 0 && lane == 0);
-                    const uint32_t r = q * 32 + lane;
-                    if (leader) ptx::bulk_wait_group_read0();
-                    ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
-                    float* dst = cstage + h * HALF * Cfg::BM;
+                    // each warp stages and TMA-stores its own 32 rows x HALF columns (no
+                    // CTA-wide barrier: a warp moves on to the next tile's drains at once)
+                    float* dst = cstage + e * (32 * HALF);
+                    if (lane == 0) ptx::bulk_wait_group_read0();   // this warp's previous store read its block
+                    __syncwarp();
 #pragma unroll
-                    for (int jj = 0; jj < HALF; ++jj) dst[jj * Cfg::BM + r] = fmaf(p.alpha, creg[jj], 0.0f);
+                    for (int jj = 0; jj < HALF; ++jj) dst[jj * 32 + lane] = fmaf(p.alpha, creg[jj], 0.0f);
                     ptx::fence_proxy_async_smem();
-                    ptx::named_bar_sync(1, Cfg::NUM_EPI_WARPS * 32);
-                    if (leader) {
-#pragma unroll
-                        for (int c = 0; c < Cfg::BN / 32; ++c)
-                            ptx::tma_store_3d(&tmC, cstage + c * 32 * Cfg::BM, mrow0, nt * Cfg::BN + c * 32, b);
+                    __syncwarp();
+                    if (lane == 0) {   // box: 32 rows x HALF columns
+                        ptx::tma_store_3d(&tmC, dst, mrow0 + (int)(q * 32), nt * Cfg::BN + (int)(h * HALF), b);
                         ptx::bulk_commit_group();
                     }
                 } else {
@@ -588,11 +605,16 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     }
                 }
                 PROF_ADD(P_EPI_STORE);
+                if (lane == 0) TRACE_AT(3 + e, 15, j);
             }
         }
-        if (p.tma_store && warp == Cfg::EPI_WARP0 && lane == 0) ptx::bulk_wait_group0();
+        if (p.tma_store && lane == 0) ptx::bulk_wait_group0();
     }
 #ifdef EMU_PROF
+    if (lane == 0 && warp == 0) TRACE_END(0);
+    if (lane == 0 && warp == 1) TRACE_END(1);
+    if (lane == 0 && warp == Cfg::SPLIT_WARP0) TRACE_END(2);
+    if (lane == 0 && warp >= Cfg::EPI_WARP0) TRACE_END(3 + warp - Cfg::EPI_WARP0);
     if (warp == 0 || warp == 1 || warp >= 4 || lane == 0) {
         prof_acc[P_CTA_TOTAL] = (warp == 4 && lane == 0) ? (unsigned long long)(clock64() - prof_start) : 0;
         if (warp != 2 && warp != 3) PROF_FLUSH();

@@ -59,7 +59,28 @@ __device__ unsigned long long g_prof[16];
             for (int i_ = 0; i_ < P_NSLOTS; ++i_)                               \
                 if (prof_acc[i_]) atomicAdd(&g_prof[i_], prof_acc[i_]);         \
     } while (0)
+// event trace of CTA 0 (the leader of cluster 0): per recording warp a region of
+// TRACE_R entries (clock64, event << 32 | arg), written without atomics
+constexpr int TRACE_ROLES = 20, TRACE_R = 1 << 12, TRACE_N = TRACE_ROLES * TRACE_R;
+__device__ long long g_trace[TRACE_N][2];
+__device__ unsigned int g_trace_cnt[TRACE_ROLES];
+#define TRACE_DECL unsigned trace_i = 0;
+#define TRACE_AT(role, ev, arg)                                                                \
+    do {                                                                                      \
+        if (blockIdx.x == 0 && trace_i < (unsigned)TRACE_R) {                                 \
+            long long* e_ = g_trace[(role) * TRACE_R + trace_i++];                            \
+            e_[0] = clock64();                                                                \
+            e_[1] = ((long long)(ev) << 32) | (unsigned)(arg);                                \
+        }                                                                                     \
+    } while (0)
+#define TRACE_END(role)                                                                       \
+    do {                                                                                      \
+        if (blockIdx.x == 0) g_trace_cnt[role] = trace_i;                                     \
+    } while (0)
 #else
+#define TRACE_DECL
+#define TRACE_AT(role, ev, arg) ((void)0)
+#define TRACE_END(role) ((void)0)
 #define PROF_DECL
 #define PROF_T0() ((void)0)
 #define PROF_ADD(slot) ((void)0)
