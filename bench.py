@@ -330,21 +330,30 @@ def main():
 
     peaks = _peaks()
     tc_peak = peaks["bf16_tflops"] * (1.0 if mode == "fp16" else 0.5)   # fp16 = bf16 rate; tf32 = 1/2 (nominal ratio)
+    # c3 runs tens of ms per launch at full tensor load (power-capped like the sustained
+    # cuBLAS measurement): its roofline uses the sustained peak; the burst fraction is
+    # reported beside it
+    tc_peak_sus = peaks["bf16_tflops_sustained"] * (1.0 if mode == "fp16" else 0.5)
+    kname = ("emu_sgemm_pair_ts_kernel<%s, 128 cols, split commit%s>"
+             % ("FP16" if mode == "fp16" else "TF32",
+                ", A-stationary" if (args.config == "c2" and (mode == "fp16" or k <= 128)) else ""))
     if args.config == "c2":
         bytes_launch = 4.0 * (m * k + k * n + m * n) * batch
         achieved = bytes_launch / (ms_per_step / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(args.config, mode),
                 "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peaks["source"],
-                "kernel": "emu_sgemm_kernel"}
+                "kernel": kname}
     else:
         tc_flops = 6.0 * m * n * k * batch
         achieved = tc_flops / (ms_per_step / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
-                "frac": achieved / tc_peak, "traffic": _traffic(args.config, mode),
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tc_peak_sus, "unit": "TFLOP/s",
+                "frac": achieved / tc_peak_sus, "frac_of_burst_peak": achieved / tc_peak,
+                "burst_peak": tc_peak, "traffic": _traffic(args.config, mode),
                 "algorithmic_flops_per_launch": tc_flops, "peak_source": peaks["source"] +
-                (" (bf16 peak; fp16 same rate)" if mode == "fp16" else " (bf16 peak x 1/2 nominal tf32 ratio)"),
-                "kernel": "emu_sgemm_kernel"}
+                (" sustained bf16 peak (fp16 same rate)" if mode == "fp16"
+                 else " sustained bf16 peak x 1/2 (nominal tf32 ratio)"),
+                "kernel": kname}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -358,6 +367,7 @@ def main():
         "config": _config(cfg, mode, world),
         "frac_fp32_simt_peak": per_gpu / FP32_SIMT_PEAK_TF,
         "frac_tc_peak_over_3": per_gpu / (tc_peak / 3.0),
+        "frac_tc_sustained_peak_over_3": per_gpu / (tc_peak_sus / 3.0),
         "rel_frobenius_vs_fp64": e_emu, "rel_frobenius_fp32_sgemm": e_sg, "accuracy_sample": acc_note,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "paper_context": PAPER_A100,

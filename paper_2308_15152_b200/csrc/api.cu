@@ -229,7 +229,7 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     p.tma_store = tma_store;
     p.prefetch = prefetch_distance();
     {
-        static const int gm = env_int("EMU_GROUP_M", 4, 1, 1 << 20);    // tuning only (measured c3: 4 > 8, 16, 32)
+        static const int gm = env_int("EMU_GROUP_M", 2, 1, 1 << 20);    // tuning only (c3 DRAM bytes: 2 < 4 < 8 < 16, profiles/r01_summary.md)
         static const int pol = env_int("EMU_L2_POLICY", 0, 0, 3);      // tuning only
         p.group_m = gm;
         p.l2_policy = pol;
@@ -298,7 +298,7 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     p.tma_store = tma_store;
     p.prefetch = prefetch_distance();
     {
-        static const int gm = env_int("EMU_GROUP_M", 4, 1, 1 << 20);    // tuning only (measured c3: 4 > 8, 16, 32)
+        static const int gm = env_int("EMU_GROUP_M", 2, 1, 1 << 20);    // tuning only (c3 DRAM bytes: 2 < 4 < 8 < 16, profiles/r01_summary.md)
         static const int pol = env_int("EMU_L2_POLICY", 0, 0, 3);      // tuning only
         p.group_m = gm;
         p.l2_policy = pol;
@@ -368,7 +368,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     p.tma_store = tma_store;
     p.prefetch = prefetch_distance();
     {
-        static const int gm = env_int("EMU_GROUP_M", 4, 1, 1 << 20);    // tuning only (measured c3: 4 > 8, 16, 32)
+        static const int gm = env_int("EMU_GROUP_M", 2, 1, 1 << 20);    // tuning only (c3 DRAM bytes: 2 < 4 < 8 < 16, profiles/r01_summary.md)
         static const int pol = env_int("EMU_L2_POLICY", 0, 0, 3);      // tuning only
         p.group_m = gm;
         p.l2_policy = pol;
