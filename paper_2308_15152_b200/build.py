@@ -30,7 +30,8 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC, *FLAGS, "-o", LIB, *SOURCES]
+        # EMU_BUILD_DEFS: extra -D flags for tuning experiments (tools/gpu_defab.sh)
+        cmd = [NVCC, *FLAGS, *os.environ.get("EMU_BUILD_DEFS", "").split(), "-o", LIB, *SOURCES]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

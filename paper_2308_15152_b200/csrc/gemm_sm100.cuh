@@ -64,6 +64,7 @@ __device__ unsigned long long g_prof[16];
 constexpr int TRACE_ROLES = 20, TRACE_R = 1 << 12, TRACE_N = TRACE_ROLES * TRACE_R;
 __device__ long long g_trace[TRACE_N][2];
 __device__ unsigned int g_trace_cnt[TRACE_ROLES];
+#ifdef EMU_TRACE
 #define TRACE_DECL unsigned trace_i = 0;
 #define TRACE_AT(role, ev, arg)                                                                \
     do {                                                                                      \
@@ -77,6 +78,11 @@ __device__ unsigned int g_trace_cnt[TRACE_ROLES];
     do {                                                                                      \
         if (blockIdx.x == 0) g_trace_cnt[role] = trace_i;                                     \
     } while (0)
+#else
+#define TRACE_DECL
+#define TRACE_AT(role, ev, arg) ((void)0)
+#define TRACE_END(role) ((void)0)
+#endif
 #else
 #define TRACE_DECL
 #define TRACE_AT(role, ev, arg) ((void)0)

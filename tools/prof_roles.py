@@ -24,7 +24,8 @@ def build():
     flags = list(B.FLAGS)
     i = flags.index("-Xptxas")
     del flags[i:i + 2]
-    cmd = [B.NVCC, *flags, "-DEMU_PROF", "-o", LIB, *B.SOURCES]
+    extra = os.environ.get("EMU_EXTRA_DEFS", "").split()   # e.g. -DEMU_TS_MMA_WARP=3 (experiments)
+    cmd = [B.NVCC, *flags, "-DEMU_PROF", *extra, "-o", LIB, *B.SOURCES]
     subprocess.check_call(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
 
 

@@ -25,6 +25,7 @@ NAMES = {1: "prod_issue", 2: "spl_got_f32", 3: "spl_got_op", 4: "spl_done", 5: "
 def main():
     mode = 0 if (len(sys.argv) <= 1 or sys.argv[1] == "fp16") else 1
     batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+    os.environ["EMU_EXTRA_DEFS"] = (os.environ.get("EMU_EXTRA_DEFS", "") + " -DEMU_TRACE").strip()
     prof_roles.build()
     L = ctypes.CDLL(prof_roles.LIB)
     m = n = k = 256
