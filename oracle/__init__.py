@@ -69,6 +69,12 @@ def lib():
         L.orc_emu_gemm_entries.argtypes = [i32, i32, i32, i32, i32, i32, f32, P, i64, i64,
                                            P, i64, i64, f32, P, i64, i64, i64, P, P, P, P]
         L.orc_emu_gemm_entries.restype = i32
+        L.orc_emu_gemm_range_batched.argtypes = L.orc_emu_gemm_batched.argtypes
+        L.orc_emu_gemm_range_batched.restype = i32
+        L.orc_emu_gemm_range_entries.argtypes = L.orc_emu_gemm_entries.argtypes
+        L.orc_emu_gemm_range_entries.restype = i32
+        L.orc_range_exponents.argtypes = [i32, i32, i32, P, i64, P, i64, P, P]
+        L.orc_range_exponents.restype = None
         L.orc_gemm_f64_batched.argtypes = [i32, i32, i32, f64, P, i64, i64, P, i64, i64,
                                            f64, P, i64, i64, P, i64, i64, i32]
         L.orc_gemm_f64_batched.restype = None
@@ -220,6 +226,56 @@ def emu_gemm_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=N
     if rc != 0:
         raise MemoryError("oracle allocation failed")
     return out
+
+
+def emu_gemm_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True, ldc=None):
+    """Range-safe mode (DESIGN R#22): per-row / per-column
+    power-of-two pre-scaling around the unchanged emulation model."""
+    mode = _MODES[mode]
+    A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
+    ldc = m if ldc is None else ldc
+    if C is None:
+        C = np.zeros((batch, n, ldc), dtype=np.float32)
+    else:
+        C = np.array(C, dtype=np.float32, copy=True).reshape(batch, n, ldc)
+    rc = lib().orc_emu_gemm_range_batched(mode, int(bool(corr)), m, n, k, kb, alpha, _p(A), lda, sA,
+                                          _p(B), ldb, sB, beta, _p(C), ldc, n * ldc, batch)
+    if rc != 0:
+        raise MemoryError("oracle allocation failed")
+    return C
+
+
+def emu_gemm_range_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=None,
+                           kb=64, corr=True, ldc=None):
+    mode = _MODES[mode]
+    A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
+    ldc = m if ldc is None else ldc
+    if C is None:
+        C = np.zeros((1, 1, 1), dtype=np.float32)
+        sC = 0
+    else:
+        C = _f32(C)
+        sC = n * ldc
+    bidx = np.ascontiguousarray(bidx, dtype=np.int64)
+    ii = np.ascontiguousarray(ii, dtype=np.int64)
+    jj = np.ascontiguousarray(jj, dtype=np.int64)
+    out = np.empty(len(ii), dtype=np.float32)
+    rc = lib().orc_emu_gemm_range_entries(mode, int(bool(corr)), m, n, k, kb, alpha, _p(A), lda, sA,
+                                          _p(B), ldb, sB, beta, _p(C), ldc, sC, len(ii),
+                                          _p(bidx), _p(ii), _p(jj), _p(out))
+    if rc != 0:
+        raise MemoryError("oracle allocation failed")
+    return out
+
+
+def range_exponents(A, B, m, n, k):
+    """(e_rows[m], f_cols[n]) of one column-major problem (A: (k, lda), B: (n, ldb))."""
+    A = _f32(A)
+    B = _f32(B)
+    e = np.empty(m, dtype=np.int32)
+    f = np.empty(n, dtype=np.int32)
+    lib().orc_range_exponents(m, n, k, _p(A), A.shape[-1], _p(B), B.shape[-1], _p(e), _p(f))
+    return e, f
 
 
 def gemm_f64(A, B, m, n, k, alpha=1.0, beta=0.0, C=None, ldc=None):

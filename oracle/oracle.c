@@ -23,6 +23,10 @@
  *                       the paper's accuracy claim (<= FP32 SGEMM level)
  *   orc_gemm_f64        exact integer product; numpy float64 matmul
  *   orc_sgemm_f32       exact integer product; gamma_k |A||B| error bound
+ *   orc_emu_gemm_range  exponent closed forms; equals the plain model when all
+ *                       exponents are 0; exact scale equivariance (row i of A
+ *                       times 2^t => row i of C times 2^t, bit for bit); small
+ *                       integers exact; the accuracy gate on 2^-30..2^30 inputs
  * Parity unpinned: none of the functions above.
  *
  * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -fPIC
@@ -391,6 +395,127 @@ int orc_emu_gemm_entries(int mode, int corr_enable, int m, int n, int k, int kb,
             }
         }
         free(ah); free(al); free(bh); free(bl);
+    }
+    return ok;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Range-safe mode (DESIGN R#22).  The paper applies    */
+/* Eqs. corr-1..4 to the raw values, so FP16 hi overflows for    */
+/* |x| >= 65520 (R#4).  This mode first scales row i of A by 2^-e_i and      */
+/* column j of B by 2^-f_j (exact power-of-two scaling):                     */
+/*   e = clamp(ilogb(max finite |x| of the row/column) - 14, -125, 125),     */
+/*       e = 0 when the row/column has no finite non-zero value,             */
+/* so the largest scaled magnitude lies in [2^14, 2^15); then runs the       */
+/* unchanged emulation (Eqs. corr-1..5 with the per-k-block combine) on      */
+/* A' = A 2^-e, B' = B 2^-f, and undoes the scaling on C_reg:                */
+/*   C(i,j) = RN(alpha * ((C'(i,j) * 2^f_j) * 2^e_i) + RN(beta * C0(i,j))).   */
+/* Each scaling is one correctly rounded ldexpf (exact unless the result is  */
+/* subnormal or overflows).                                                  */
+/* ------------------------------------------------------------------------ */
+static int range_exp(const float* x, int64_t count, int64_t stride)
+{
+    float mx = 0.0f;
+    for (int64_t p = 0; p < count; ++p) {
+        float v = fabsf(x[p * stride]);
+        if (isfinite(v) && v > mx) mx = v;
+    }
+    if (mx == 0.0f) return 0;
+    int e = ilogbf(mx) - 14;
+    return e < -125 ? -125 : (e > 125 ? 125 : e);
+}
+
+/* exponents of the m rows of A (column-major, lda) and the n columns of B */
+void orc_range_exponents(int m, int n, int k, const float* A, int64_t lda,
+                         const float* B, int64_t ldb, int* e_rows, int* f_cols)
+{
+    for (int i = 0; i < m; ++i) e_rows[i] = range_exp(A + i, k, lda);
+    for (int j = 0; j < n; ++j) f_cols[j] = range_exp(B + (int64_t)j * ldb, k, 1);
+}
+
+static float range_unscale(float alpha, float c_reg, int f, int e, float bc)
+{
+    return fmaf(alpha, ldexpf(ldexpf(c_reg, f), e), bc);
+}
+
+int orc_emu_gemm_range_batched(int mode, int corr_enable, int m, int n, int k, int kb,
+                               float alpha, const float* A, int64_t lda, int64_t strideA,
+                               const float* B, int64_t ldb, int64_t strideB,
+                               float beta, float* C, int64_t ldc, int64_t strideC,
+                               int batch)
+{
+    if (kb <= 0) kb = 64;
+    int64_t mk = (int64_t)m * k, kn = (int64_t)k * n, mn = (int64_t)m * n;
+    float* As = malloc(sizeof(float) * (mk > 0 ? mk : 1));
+    float* Bs = malloc(sizeof(float) * (kn > 0 ? kn : 1));
+    float* Cr = malloc(sizeof(float) * (mn > 0 ? mn : 1));
+    int* e = malloc(sizeof(int) * (m > 0 ? m : 1));
+    int* f = malloc(sizeof(int) * (n > 0 ? n : 1));
+    if (!As || !Bs || !Cr || !e || !f) { free(As); free(Bs); free(Cr); free(e); free(f); return -1; }
+    int rc = 0;
+    for (int b = 0; b < batch && rc == 0; ++b) {
+        const float* Ab = A + (int64_t)b * strideA;
+        const float* Bb = B + (int64_t)b * strideB;
+        float* Cb = C + (int64_t)b * strideC;
+        orc_range_exponents(m, n, k, Ab, lda, Bb, ldb, e, f);
+        for (int p = 0; p < k; ++p)                       /* A' (m x k, ld m) */
+            for (int i = 0; i < m; ++i) As[i + (int64_t)p * m] = ldexpf(Ab[i + (int64_t)p * lda], -e[i]);
+        for (int j = 0; j < n; ++j)                       /* B' (k x n, ld k) */
+            for (int p = 0; p < k; ++p) Bs[p + (int64_t)j * k] = ldexpf(Bb[p + (int64_t)j * ldb], -f[j]);
+        /* C_reg' = the unchanged emulation of A' B' (alpha = 1, beta = 0: fmaf(1, C, 0) = C) */
+        rc = orc_emu_gemm_batched(mode, corr_enable, m, n, k, kb, 1.0f, As, m, 0, Bs, k, 0,
+                                  0.0f, Cr, m, 0, 1);
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < m; ++i) {
+                float bc = (beta != 0.0f) ? beta * Cb[i + (int64_t)j * ldc] : 0.0f;
+                Cb[i + (int64_t)j * ldc] = (alpha == 0.0f || k == 0)
+                    ? bc : range_unscale(alpha, Cr[i + (int64_t)j * m], f[j], e[i], bc);
+            }
+    }
+    free(As); free(Bs); free(Cr); free(e); free(f);
+    return rc;
+}
+
+/* selected entries of the range-safe GEMM (sampled parity at full sizes) */
+int orc_emu_gemm_range_entries(int mode, int corr_enable, int m, int n, int k, int kb,
+                               float alpha, const float* A, int64_t lda, int64_t strideA,
+                               const float* B, int64_t ldb, int64_t strideB,
+                               float beta, const float* C, int64_t ldc, int64_t strideC,
+                               int64_t nent, const int64_t* bidx, const int64_t* ii,
+                               const int64_t* jj, float* out)
+{
+    (void)m; (void)n;
+    if (kb <= 0) kb = 64;
+    int ok = 0;
+    #pragma omp parallel
+    {
+        size_t kk = (size_t)(k > 0 ? k : 1);
+        float* a = malloc(sizeof(float) * kk);
+        float* bcol = malloc(sizeof(float) * kk);
+        float* ah = malloc(sizeof(float) * kk);
+        float* al = malloc(sizeof(float) * kk);
+        float* bh = malloc(sizeof(float) * kk);
+        float* bl = malloc(sizeof(float) * kk);
+        if (!a || !bcol || !ah || !al || !bh || !bl) {
+            #pragma omp atomic write
+            ok = -1;
+        } else {
+            #pragma omp for schedule(dynamic, 4)
+            for (int64_t t = 0; t < nent; ++t) {
+                const float* Ab = A + bidx[t] * strideA;
+                const float* Bb = B + bidx[t] * strideB;
+                int e = range_exp(Ab + ii[t], k, lda);
+                int f = range_exp(Bb + jj[t] * ldb, k, 1);
+                for (int p = 0; p < k; ++p) a[p] = ldexpf(Ab[ii[t] + (int64_t)p * lda], -e);
+                for (int p = 0; p < k; ++p) bcol[p] = ldexpf(Bb[(int64_t)p + jj[t] * ldb], -f);
+                split_row(mode, k, a, 1, 0, ah, al);
+                split_col(mode, k, bcol, k, 0, bh, bl);
+                float c_reg = emu_element(mode, corr_enable, k, kb, ah, al, bh, bl, 1.0f, 0.0f, 0.0f, 0);
+                float bc = (beta != 0.0f) ? beta * C[bidx[t] * strideC + ii[t] + jj[t] * ldc] : 0.0f;
+                out[t] = (alpha == 0.0f || k == 0) ? bc : range_unscale(alpha, c_reg, f, e, bc);
+            }
+        }
+        free(a); free(bcol); free(ah); free(al); free(bh); free(bl);
     }
     return ok;
 }

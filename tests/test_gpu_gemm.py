@@ -212,6 +212,28 @@ def test_accuracy_gate_vs_fp64(mode, k):
         assert e_gpu <= 2 * e_sg and e_gpu <= 1e-5, (e_gpu, e_sg)
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_accuracy_vs_cublas_sgemm(mode):
+    """SURVEY §8(c) pin 5: the method is as accurate as cuBLAS SGEMM on the same GPU
+    (torch FP32 matmul with TF32 disabled), relative Frobenius vs FP64."""
+    import torch
+    m = n = 256
+    k = 4096
+    A, B = workloads.make_operands(1, m, n, k, seed=61)
+    R = oracle.gemm_f64(A, B, m, n, k)
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        Am = torch.from_numpy(A[0]).cuda().T    # column-major (k, m) storage -> m x k
+        Bm = torch.from_numpy(B[0]).cuda().T    # (n, k) storage -> k x n
+        Cc = (Am @ Bm).T.contiguous().cpu().numpy()[None]   # back to (n, m) storage
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+    e_cublas = oracle.rel_frobenius(Cc, R)
+    e_gpu = oracle.rel_frobenius(emu_gpu(mode, A, B, m, n, k), R)
+    assert e_gpu <= 2 * e_cublas, (e_gpu, e_cublas)
+
+
 def test_c4_stress_range():
     """c4 (k = 4096, magnitudes 2^-30..2^30): FP16 mode overflows (R#4) and the
     range flag reports it; TF32 mode passes the accuracy gate."""
