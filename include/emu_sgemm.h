@@ -34,7 +34,8 @@
  * surface as CUDA errors at the caller's next synchronisation.
  *
  * Memory: the device entries allocate no global memory (tensor memory is
- * allocated and freed inside each CTA); per-device attributes are cached.
+ * allocated and freed inside each CTA; the range-safe entry uses a caller-owned
+ * workspace); per-device attributes are cached.
  * Thread-safe.  sm_100a only (B200); other devices -> EMU_STATUS_ARCH_MISMATCH.
  */
 #ifndef EMU_SGEMM_H_
@@ -106,6 +107,38 @@ emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha,
                                 float beta, float* C, int ldc, long long strideC,
                                 int batch, emu_split_mode mode, void* stream,
                                 unsigned int* d_range_flag, int kblock, unsigned int flags);
+
+/*
+ * Range-safe mode (DESIGN R#22).  The paper splits raw
+ * values, so FP16 mode overflows for |x| >= 65520 (R#4).  This
+ * entry first scales row i of A_b by 2^-e_i and column j of B_b by 2^-f_j,
+ *   e = clamp(ilogb(max finite |x| over the row / column) - 14, -125, 125)
+ *   (0 when the row / column has no finite non-zero element),
+ * so every scaled row / column peaks in [2^14, 2^15); runs the unchanged
+ * method (split, three products, per-k-block combine) on the scaled operands;
+ * and un-scales the combined accumulator: C = RN(alpha*((C'*2^f_j)*2^e_i) +
+ * RN(beta*C)).  Power-of-two scaling is exact except where a scaled value is
+ * subnormal or overflows.  The exponents come from one max-|x| pass over A
+ * and B (a second kernel, recorded by emu_last_launch_count).
+ *
+ * emu_range_workspace_size: bytes of device workspace the call needs,
+ *   4 * batch * (m + n) (returns 0 for negative arguments).
+ * emu_sgemm_batched_range: arguments as emu_sgemm_batched_ex, plus
+ *   d_workspace / workspace_bytes: caller-owned device memory, 16-byte aligned,
+ *     >= emu_range_workspace_size(m, n, batch); not aliased with A, B, C; it may
+ *     be reused once the call's work on `stream` has completed.
+ *   Errors: as emu_sgemm_batched_ex; workspace NULL, misaligned or too small ->
+ *   EMU_STATUS_INVALID_VALUE; operands outside the TMA domain (base not 16-byte
+ *   aligned, lda/ldb/strides not multiples of 4) -> EMU_STATUS_NOT_SUPPORTED.
+ */
+size_t emu_range_workspace_size(int m, int n, int batch);
+emu_status emu_sgemm_batched_range(int m, int n, int k, float alpha,
+                                   const float* A, int lda, long long strideA,
+                                   const float* B, int ldb, long long strideB,
+                                   float beta, float* C, int ldc, long long strideC,
+                                   int batch, emu_split_mode mode, void* stream,
+                                   void* d_workspace, size_t workspace_bytes,
+                                   unsigned int* d_range_flag, int kblock, unsigned int flags);
 
 /*
  * emu_sgemm_batched_host -- the same operation on HOST buffers (pinned or

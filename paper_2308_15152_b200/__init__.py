@@ -49,6 +49,10 @@ lib.emu_sgemm_batched.argtypes = _GEMM_ARGS
 lib.emu_sgemm_batched.restype = _i
 lib.emu_sgemm_batched_ex.argtypes = _GEMM_ARGS + [_p, _i, _u]
 lib.emu_sgemm_batched_ex.restype = _i
+lib.emu_sgemm_batched_range.argtypes = _GEMM_ARGS + [_p, ctypes.c_size_t, _p, _i, _u]
+lib.emu_sgemm_batched_range.restype = _i
+lib.emu_range_workspace_size.argtypes = [_i, _i, _i]
+lib.emu_range_workspace_size.restype = ctypes.c_size_t
 lib.emu_sgemm_batched_host.argtypes = _GEMM_ARGS
 lib.emu_sgemm_batched_host.restype = _i
 lib.emu_sgemm.argtypes = [_i, _i, _i, _f, _p, _i, _p, _i, _f, _p, _i, _i, _p]
@@ -110,6 +114,19 @@ def emu_sgemm_batched_ex(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
                                     beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream),
                                     _ptr(range_flag), kblock, flags),
            "emu_sgemm_batched_ex")
+
+
+def emu_range_workspace_size(m, n, batch) -> int:
+    return int(lib.emu_range_workspace_size(m, n, batch))
+
+
+def emu_sgemm_batched_range(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+                            batch, mode, workspace, workspace_bytes, stream=None, range_flag=None, kblock=0,
+                            flags=0):
+    _check(lib.emu_sgemm_batched_range(m, n, k, alpha, _ptr(A), lda, strideA, _ptr(B), ldb, strideB,
+                                       beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream),
+                                       _ptr(workspace), workspace_bytes, _ptr(range_flag), kblock, flags),
+           "emu_sgemm_batched_range")
 
 
 def emu_sgemm_batched_host(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,

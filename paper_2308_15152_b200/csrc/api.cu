@@ -122,6 +122,43 @@ __global__ void scale_c_kernel(float* C, int m, int n, long long ldc, long long 
     }
 }
 
+// range-safe mode (R#22): bit patterns of the max finite |x| of every row of A_b and
+// column of B_b (non-negative binary32 values order like their bit patterns, so an
+// integer atomicMax merges the k-chunks).  blockIdx.x: (item, A row block of 256 | B
+// column block of 8 warps), blockIdx.y: k-chunk.
+__global__ void range_max_kernel(const float* __restrict__ A, long long lda, long long strideA,
+                                 const float* __restrict__ B, long long ldb, long long strideB, int m, int n, int k,
+                                 int a_blocks, int b_blocks, int kchunk, unsigned* __restrict__ row_max,
+                                 unsigned* __restrict__ col_max)
+{
+    const int per_item = a_blocks + b_blocks;
+    const long long item = blockIdx.x / per_item;
+    const int blk = (int)(blockIdx.x - item * per_item);
+    const int p0 = blockIdx.y * kchunk, p1 = min(k, p0 + kchunk);
+    if (blk < a_blocks) {
+        const int r = blk * 256 + (int)threadIdx.x;
+        if (r >= m) return;
+        const float* a = A + item * strideA + r;
+        float mx = 0.0f;
+        for (int p = p0; p < p1; ++p) {
+            const float v = fabsf(__ldg(a + (long long)p * lda));
+            if (v <= 3.402823466e38f) mx = fmaxf(mx, v);   // finite values only (NaN compares false)
+        }
+        if (mx > 0.0f) atomicMax(row_max + item * m + r, __float_as_uint(mx));
+    } else {
+        const int c = (blk - a_blocks) * 8 + (int)(threadIdx.x >> 5);
+        if (c >= n) return;
+        const float* bcol = B + item * strideB + (long long)c * ldb;
+        float mx = 0.0f;
+        for (int p = p0 + (int)(threadIdx.x & 31); p < p1; p += 32) {
+            const float v = fabsf(__ldg(bcol + p));
+            if (v <= 3.402823466e38f) mx = fmaxf(mx, v);
+        }
+        const unsigned bits = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+        if ((threadIdx.x & 31) == 0 && bits) atomicMax(col_max + item * n + c, bits);
+    }
+}
+
 __global__ void split_fp16_kernel(const float* __restrict__ x, long long count, uint16_t* __restrict__ hi,
                                   uint16_t* __restrict__ lo)
 {
@@ -315,7 +352,7 @@ template <int MODE, bool RANGE, int BN, bool SPLITC, bool ASTAT>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
-                         unsigned flags)
+                         unsigned flags, const unsigned* row_max, const unsigned* col_max)
 {
     using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT>;
     {
@@ -374,6 +411,8 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
         p.l2_policy = pol;
     }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
+    p.row_max = row_max;
+    p.col_max = col_max;
     p.num_units = ASTAT ? (long long)p.tiles_m * batch : p.num_tiles;
     p.unit_tiles = ASTAT ? p.tiles_n : 1;
     if (ASTAT && p.num_k_stages > Cfg::ASLOTS) return EMU_STATUS_NOT_SUPPORTED;   // dispatch guarantees it
@@ -405,10 +444,12 @@ __attribute__((visibility("default"))) int emu_version(void) { return EMU_VERSIO
 
 __attribute__((visibility("default"))) int emu_last_launch_count(void) { return g_last_launches; }
 
-__attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
-                                const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
-                                long long strideC, int batch, emu_split_mode mode, void* stream,
-                                unsigned int* d_range_flag, int kblock, unsigned int flags)
+// the device entries; range_ws != nullptr selects the range-safe mode (R#22)
+static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
+                            const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
+                            long long strideC, int batch, emu_split_mode mode, void* stream,
+                            unsigned int* d_range_flag, int kblock, unsigned int flags, void* range_ws,
+                            size_t range_ws_bytes)
 {
     g_last_launches = 0;
     // ---- synchronous validation (C untouched on error) ----
@@ -423,6 +464,9 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     if (batch > 1 && strideC < (long long)ldc * n) return EMU_STATUS_INVALID_VALUE;
     const bool reads_ab = k > 0 && alpha != 0.0f;
     if (reads_ab && (A == nullptr || B == nullptr)) return EMU_STATUS_INVALID_VALUE;
+    const bool range = range_ws != nullptr;
+    if (range && (!aligned16(range_ws) || range_ws_bytes < (size_t)4 * (size_t)batch * ((size_t)m + (size_t)n)))
+        return EMU_STATUS_INVALID_VALUE;
 
     int dev = 0, sms = 0;
     emu_status st = device_check(dev, sms);
@@ -446,6 +490,24 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
         return e && strcmp(e, "1") == 0;
     }();
     const bool ldg = !tma_ok || force_ldg;
+    const unsigned* row_max = nullptr;
+    const unsigned* col_max = nullptr;
+    if (range) {
+        // range-safe mode: TS kernel only (any m); exponents from one max-|x| pass
+        if (!tma_ok) return EMU_STATUS_NOT_SUPPORTED;
+        unsigned* ws = static_cast<unsigned*>(range_ws);
+        if (cudaMemsetAsync(ws, 0, (size_t)4 * batch * ((size_t)m + n), s) != cudaSuccess)
+            return EMU_STATUS_CUDA_ERROR;
+        const int a_blocks = (m + 255) / 256, b_blocks = (n + 7) / 8, kchunk = 512;
+        const dim3 grid((unsigned)((long long)batch * (a_blocks + b_blocks)), (unsigned)((k + kchunk - 1) / kchunk));
+        const long long sAr = batch > 1 ? strideA : 0, sBr = batch > 1 ? strideB : 0;
+        range_max_kernel<<<grid, 256, 0, s>>>(A, lda, sAr, B, ldb, sBr, m, n, k, a_blocks, b_blocks, kchunk, ws,
+                                              ws + (size_t)batch * m);
+        const emu_status ls = launch_status(cudaGetLastError());
+        if (ls != EMU_STATUS_SUCCESS) return ls;
+        row_max = ws;
+        col_max = ws + (size_t)batch * m;
+    }
     // CTA-pair kernel for problems with more than one 128-row block
     static const int kernel_pref = [] {
         const char* e = getenv("EMU_KERNEL");   // "single" | "pair" | "ts": tuning/diagnostics only
@@ -457,7 +519,7 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     // A-in-TMEM pair kernel (fewest shared-memory bytes per MMA) for every problem
     // with more than one 128-row block; the SMEM-operand pair kernel stays selectable
     // (EMU_KERNEL=pair) for comparison.
-    const bool ts = !ldg && (kernel_pref == 3 || (kernel_pref == 0 && m > 128));
+    const bool ts = !ldg && (range || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     // tile width of the TS kernel (profiles/r01_summary.md): 128 with one accumulator
     // buffer whose D_corr and D_hi drains overlap the other part's MMAs (SPLITC); the
@@ -478,27 +540,31 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
 #define EMU_RUN_TS(MODE_, RANGE_)                                                                                      \
     do {                                                                                                               \
         if (ts_as)                                                                                                     \
-            return run_gemm_pair_ts<MODE_, RANGE_, 128, true, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, \
+            { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, \
                                                                     strideB, beta, C, ldc, strideC, batch, s,          \
-                                                                    d_range_flag, kblock, flags);                      \
+                                                                    d_range_flag, kblock, flags, row_max, col_max); break; }    \
         if (ts_sc)                                                                                                     \
-            return run_gemm_pair_ts<MODE_, RANGE_, 128, true, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,     \
+            { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,     \
                                                                      ldb, strideB, beta, C, ldc, strideC, batch, s,    \
-                                                                     d_range_flag, kblock, flags);                     \
+                                                                     d_range_flag, kblock, flags, row_max, col_max); break; }   \
         if (ts_n == 128)                                                                                               \
-            return run_gemm_pair_ts<MODE_, RANGE_, 128, false, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,    \
+            { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, false, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,    \
                                                                       ldb, strideB, beta, C, ldc, strideC, batch, s,   \
-                                                                      d_range_flag, kblock, flags);                    \
-        return run_gemm_pair_ts<MODE_, RANGE_, 96, false, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,    \
+                                                                      d_range_flag, kblock, flags, row_max, col_max); break; }  \
+        { rs = run_gemm_pair_ts<MODE_, RANGE_, 96, false, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,    \
                                                                  strideB, beta, C, ldc, strideC, batch, s,             \
-                                                                 d_range_flag, kblock, flags);                         \
+                                                                 d_range_flag, kblock, flags, row_max, col_max); break; }       \
     } while (0)
     if (ts) {
+        emu_status rs;
         if (mode == EMU_SPLIT_FP16) {
             if (d_range_flag) EMU_RUN_TS(0, true);
-            EMU_RUN_TS(0, false);
+            else EMU_RUN_TS(0, false);
+        } else {
+            EMU_RUN_TS(1, false);
         }
-        EMU_RUN_TS(1, false);
+        if (range && rs == EMU_STATUS_SUCCESS) g_last_launches = 2;   // max-|x| pass + GEMM
+        return rs;
     }
 #undef EMU_RUN_TS
 #define EMU_RUN_PAIR(MODE_, ALAY_, RANGE_)                                                                          \
@@ -531,6 +597,32 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
     if (tf32_mn) EMU_RUN(1, emu::A_MN_SW128_32B, false, false);
     EMU_RUN(1, emu::A_K_SW128, false, false);
 #undef EMU_RUN
+}
+
+__attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
+                                const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
+                                long long strideC, int batch, emu_split_mode mode, void* stream,
+                                unsigned int* d_range_flag, int kblock, unsigned int flags)
+{
+    return gemm_impl(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, mode, stream,
+                     d_range_flag, kblock, flags, nullptr, 0);
+}
+
+__attribute__((visibility("default"))) size_t emu_range_workspace_size(int m, int n, int batch)
+{
+    if (m < 0 || n < 0 || batch < 0) return 0;
+    return (size_t)4 * (size_t)batch * ((size_t)m + (size_t)n);
+}
+
+__attribute__((visibility("default"))) emu_status emu_sgemm_batched_range(int m, int n, int k, float alpha, const float* A, int lda,
+                                   long long strideA, const float* B, int ldb, long long strideB, float beta,
+                                   float* C, int ldc, long long strideC, int batch, emu_split_mode mode,
+                                   void* stream, void* d_workspace, size_t workspace_bytes,
+                                   unsigned int* d_range_flag, int kblock, unsigned int flags)
+{
+    if (d_workspace == nullptr) return EMU_STATUS_INVALID_VALUE;
+    return gemm_impl(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, mode, stream,
+                     d_range_flag, kblock, flags, d_workspace, workspace_bytes);
 }
 
 __attribute__((visibility("default"))) emu_status emu_sgemm_batched(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,

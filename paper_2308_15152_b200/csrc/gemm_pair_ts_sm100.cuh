@@ -351,6 +351,16 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         for (long long u = cid; u < num_units; u += ncl, ++unit_it) {
             for (int j = 0; j < R; ++j) {
                 const bool doA = !ASTAT || j == 0;
+                // range-safe mode: this thread's row of A and column of B scale by 2^-e
+                float sa = 1.0f, sb = 1.0f;
+                if (p.row_max) {
+                    int b, mt, nt;
+                    ts_unit_tile<ASTAT>(p, u, j, b, mt, nt);
+                    const int r = mt * 256 + (int)rank * Cfg::BM + (int)m;
+                    const int c = nt * Cfg::BN + (int)rank * Cfg::BNC + (int)n;
+                    if (r < p.m) sa = pow2i(-range_exp_of(p.row_max[(long long)b * p.m + r]));
+                    if (has_b && c < p.n) sb = pow2i(-range_exp_of(p.col_max[(long long)b * p.n + c]));
+                }
                 for (int ks = 0; ks < nks; ++ks) {
                     // operand slot first, then the FP32 stage: a stage is held only while it
                     // is split, so the producer keeps the whole FP32 ring in flight
@@ -381,6 +391,19 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll
                         for (int c = 0; c < 2; ++c)
                             vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
+                    }
+                    if (p.row_max) {   // exact power-of-two scaling (RN where the result is subnormal)
+                        if (doA) {
+#pragma unroll
+                            for (int jj = 0; jj < Cfg::KS; ++jj) av[jj] = __fmul_rn(av[jj], sa);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            vb[c].x = __fmul_rn(vb[c].x, sb);
+                            vb[c].y = __fmul_rn(vb[c].y, sb);
+                            vb[c].z = __fmul_rn(vb[c].z, sb);
+                            vb[c].w = __fmul_rn(vb[c].w, sb);
+                        }
                     }
                     // ---- A: split into TMEM columns (lane = m)
                     if (doA) {
@@ -571,6 +594,17 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 PROF_T0();
                 if (lane == 0) TRACE_AT(3 + e, 14, j);
                 const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
+                if (p.row_max) {   // range-safe mode: C_acc * 2^f_j * 2^e_i (exact unless out of range)
+                    const int r = mrow0 + (int)(q * 32 + lane);
+                    const float ua = r < p.m ? pow2i(range_exp_of(p.row_max[(long long)b * p.m + r])) : 1.0f;
+                    const int colb = nt * Cfg::BN + (int)(h * HALF);
+#pragma unroll
+                    for (int jj = 0; jj < HALF; ++jj) {
+                        const float ub = colb + jj < p.n
+                                             ? pow2i(range_exp_of(p.col_max[(long long)b * p.n + colb + jj])) : 1.0f;
+                        creg[jj] = __fmul_rn(__fmul_rn(creg[jj], ub), ua);
+                    }
+                }
                 if (p.tma_store) {
                     // each warp stages and TMA-stores its own 32 rows x HALF columns (no
                     // CTA-wide barrier: a warp moves on to the next tile's drains at once)

@@ -111,11 +111,27 @@ struct GemmParams {
     int group_m;                  // raster: m-tiles per group walking the n-tiles together
     int l2_policy;                // 0 default; 1 B evict_last; 2 A evict_last; 3 both
     unsigned int* range_flag;     // nullable (FP16 mode only)
+    // range-safe mode (TS kernel): max |x| bit patterns of the rows of A / columns of
+    // B, [batch][m] and [batch][n]; nullptr = unscaled (the paper's method)
+    const unsigned int* row_max;
+    const unsigned int* col_max;
     // direct-load (LDG) variant only: operands read by the splitter warps
     const float* A;
     const float* B;
     long long lda, ldb, strideA, strideB;   // elements; stride 0 = shared operand
 };
+
+// range-safe mode: exponent e = clamp(ilogb(max) - 14, -125, 125) of a row / column from
+// the bit pattern of its max finite |x| (0 for none), and 2^t for |t| <= 125
+__device__ __forceinline__ int range_exp_of(unsigned int maxbits)
+{
+    if (maxbits == 0u) return 0;
+    const int be = (int)(maxbits >> 23);
+    const int lg = be ? be - 127 : -118 - __clz(maxbits & 0x7fffffu);   // ilogb, subnormals too
+    const int e = lg - 14;
+    return e < -125 ? -125 : (e > 125 ? 125 : e);
+}
+__device__ __forceinline__ float pow2i(int t) { return __int_as_float((127 + t) << 23); }
 
 // A operand layouts in the operand ring
 enum : int {

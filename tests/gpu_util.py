@@ -58,3 +58,31 @@ def tolerance(mode, A, B, m, n, k, kblock=64):
     for b in range(batch):
         out[b] = oracle.absgemm_f64(A[b if A.shape[0] > 1 else 0], B[b if B.shape[0] > 1 else 0], m, n, k)
     return gamma * U * out
+
+
+def emu_gpu_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kblock=0, flags=0, range_flag=None):
+    """the range-safe entry (R#22) on column-major numpy operands; returns (batch, n, m)"""
+    import torch
+    import paper_2308_15152_b200 as emu
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    B = np.ascontiguousarray(B, dtype=np.float32)
+    if A.ndim == 2:
+        A = A[None]
+    if B.ndim == 2:
+        B = B[None]
+    batch = max(A.shape[0], B.shape[0])
+    lda, ldb = A.shape[2], B.shape[2]
+    sA = 0 if (A.shape[0] == 1 and batch > 1) else A.shape[1] * lda
+    sB = 0 if (B.shape[0] == 1 and batch > 1) else B.shape[1] * ldb
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    if C is None:
+        dC = torch.full((batch, n, m), float("nan"), device="cuda")
+    else:
+        dC = torch.from_numpy(np.ascontiguousarray(C, dtype=np.float32).reshape(batch, n, m)).cuda()
+    nbytes = emu.emu_range_workspace_size(m, n, batch)
+    ws = torch.empty(max(nbytes // 4, 4), dtype=torch.int32, device="cuda")
+    emu.emu_sgemm_batched_range(m, n, k, alpha, dA, lda, sA, dB, ldb, sB, beta, dC, m, n * m, batch,
+                                mode, ws, nbytes, None, range_flag, kblock, flags)
+    torch.cuda.synchronize()
+    return dC.cpu().numpy()

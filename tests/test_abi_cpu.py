@@ -96,3 +96,23 @@ def test_split_validation(emu):
     assert L.emu_split(None, 4, 0, 16, 16, None) == 1
     assert L.emu_split(18, 4, 0, 16, 16, None) == 1       # misaligned
     assert L.emu_split(None, 0, 0, None, None, None) == 0
+
+
+def test_range_entry_validation(emu):
+    """range-safe entry (R#22): workspace size and the workspace checks run
+    before any CUDA call."""
+    L = emu.lib
+    assert L.emu_range_workspace_size(256, 128, 10) == 4 * 10 * (256 + 128)
+    assert L.emu_range_workspace_size(-1, 8, 1) == 0
+    args = [8, 8, 8, 1.0, 16, 8, 0, 16, 8, 0, 0.0, 16, 8, 0, 1, 0, None]
+    need = 4 * (8 + 8)
+    assert L.emu_sgemm_batched_range(*args, None, need, None, 0, 0) == 1      # no workspace
+    assert L.emu_sgemm_batched_range(*args, 4096, need - 4, None, 0, 0) == 1  # too small
+    assert L.emu_sgemm_batched_range(*args, 4100, need, None, 0, 0) == 1     # not 16-byte aligned
+    assert L.emu_sgemm_batched_range(*args, 4096, need, None, 48, 0) == 1    # kblock
+    bad = list(args)
+    bad[0] = -1
+    assert L.emu_sgemm_batched_range(*bad, 4096, need, None, 0, 0) == 1
+    empty = list(args)
+    empty[14] = 0                                                             # batch = 0: quick return
+    assert L.emu_sgemm_batched_range(*empty, 4096, 0, None, 0, 0) == 0
