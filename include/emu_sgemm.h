@@ -109,6 +109,26 @@ emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha,
                                 unsigned int* d_range_flag, int kblock, unsigned int flags);
 
 /*
+ * emu_sgemm_batched_t -- C_b = alpha * op(A_b) op(B_b) + beta * C_b with BLAS
+ * transpose arguments (the paper's problem is C = A B):
+ *   transa 'N'/'n': op(A) = A, stored m x k (lda >= max(1, m));
+ *          'T'/'t' (or 'C'/'c', real data): op(A) = A^T, A stored k x m (lda >= max(1, k));
+ *   transb 'N': op(B) = B, stored k x n (ldb >= max(1, k));
+ *          'T': op(B) = B^T, B stored n x k (ldb >= max(1, n)).
+ * The method, the other arguments and the errors are those of emu_sgemm_batched_ex;
+ * an invalid trans character -> EMU_STATUS_INVALID_VALUE.  Transposed operands are
+ * read by TMA only: a transposed operand outside the TMA domain (base not 16-byte
+ * aligned, ld or stride not a multiple of 4) -> EMU_STATUS_NOT_SUPPORTED.
+ * ('N', 'N') is exactly emu_sgemm_batched_ex.
+ */
+emu_status emu_sgemm_batched_t(char transa, char transb, int m, int n, int k, float alpha,
+                               const float* A, int lda, long long strideA,
+                               const float* B, int ldb, long long strideB,
+                               float beta, float* C, int ldc, long long strideC,
+                               int batch, emu_split_mode mode, void* stream,
+                               unsigned int* d_range_flag, int kblock, unsigned int flags);
+
+/*
  * Range-safe mode (DESIGN R#22).  The paper splits raw
  * values, so FP16 mode overflows for |x| >= 65520 (R#4).  This
  * entry first scales row i of A_b by 2^-e_i and column j of B_b by 2^-f_j,

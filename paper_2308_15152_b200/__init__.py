@@ -49,6 +49,8 @@ lib.emu_sgemm_batched.argtypes = _GEMM_ARGS
 lib.emu_sgemm_batched.restype = _i
 lib.emu_sgemm_batched_ex.argtypes = _GEMM_ARGS + [_p, _i, _u]
 lib.emu_sgemm_batched_ex.restype = _i
+lib.emu_sgemm_batched_t.argtypes = [ctypes.c_char, ctypes.c_char] + _GEMM_ARGS + [_p, _i, _u]
+lib.emu_sgemm_batched_t.restype = _i
 lib.emu_sgemm_batched_range.argtypes = _GEMM_ARGS + [_p, ctypes.c_size_t, _p, _i, _u]
 lib.emu_sgemm_batched_range.restype = _i
 lib.emu_range_workspace_size.argtypes = [_i, _i, _i]
@@ -114,6 +116,16 @@ def emu_sgemm_batched_ex(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta,
                                     beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream),
                                     _ptr(range_flag), kblock, flags),
            "emu_sgemm_batched_ex")
+
+
+def emu_sgemm_batched_t(transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc,
+                        strideC, batch, mode, stream=None, range_flag=None, kblock=0, flags=0):
+    _check(lib.emu_sgemm_batched_t(transa.encode() if isinstance(transa, str) else transa,
+                                   transb.encode() if isinstance(transb, str) else transb,
+                                   m, n, k, alpha, _ptr(A), lda, strideA, _ptr(B), ldb, strideB,
+                                   beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream),
+                                   _ptr(range_flag), kblock, flags),
+           "emu_sgemm_batched_t")
 
 
 def emu_range_workspace_size(m, n, batch) -> int:

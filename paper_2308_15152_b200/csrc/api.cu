@@ -45,7 +45,7 @@ struct DeviceInfo {
     int sms = 0;
     bool attr_set[32] = {};
     bool pair_attr_set[16] = {};
-    bool ts_attr_set[32] = {};
+    bool ts_attr_set[128] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -348,7 +348,7 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
-template <int MODE, bool RANGE, int BN, bool SPLITC, bool ASTAT>
+template <int MODE, bool RANGE, int BN, bool SPLITC, bool ASTAT, bool TA = false, bool TB = false>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
@@ -357,10 +357,10 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT>;
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        const int slot = (((MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1)) * 2 + (SPLITC ? 1 : 0)) * 2 +
-                         (ASTAT ? 1 : 0);
+        const int slot = (((((MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1)) * 2 + (SPLITC ? 1 : 0)) * 2 +
+                           (ASTAT ? 1 : 0)) * 2 + (TA ? 1 : 0)) * 2 + (TB ? 1 : 0);
         if (!g_dev[dev].ts_attr_set[slot]) {
-            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT>,
+            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
                 return EMU_STATUS_CUDA_ERROR;
             g_dev[dev].ts_attr_set[slot] = true;
@@ -373,14 +373,18 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     std::memset(&tmA, 0, sizeof(tmA));
     std::memset(&tmB, 0, sizeof(tmB));
     std::memset(&tmC, 0, sizeof(tmC));
-    const uint64_t sA = a_b ? (uint64_t)strideA : (((uint64_t)lda * (uint64_t)k + 3) & ~uint64_t(3));
-    const uint64_t sB = b_b ? (uint64_t)strideB : (((uint64_t)ldb * (uint64_t)n + 3) & ~uint64_t(3));
-    if (!make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA, Cfg::BM, Cfg::BK,
-                  CU_TENSOR_MAP_SWIZZLE_NONE))
-        return EMU_STATUS_NOT_SUPPORTED;
-    if (!make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB, Cfg::BK, Cfg::BNC,
-                  CU_TENSOR_MAP_SWIZZLE_128B))
-        return EMU_STATUS_NOT_SUPPORTED;
+    const uint64_t sA = a_b ? (uint64_t)strideA : (((uint64_t)lda * (uint64_t)(TA ? m : k) + 3) & ~uint64_t(3));
+    const uint64_t sB = b_b ? (uint64_t)strideB : (((uint64_t)ldb * (uint64_t)(TB ? k : n) + 3) & ~uint64_t(3));
+    // op(A) = A (m x k, m contiguous) or A^T (A stored k x m); op(B) = B (k x n) or B^T (B stored n x k)
+    const bool mapA = TA ? make_map(&tmA, A, (uint64_t)k, (uint64_t)m, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA,
+                                    Cfg::BK, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_128B)
+                         : make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA,
+                                    Cfg::BM, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const bool mapB = TB ? make_map(&tmB, B, (uint64_t)n, (uint64_t)k, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB,
+                                    Cfg::BNC, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
+                         : make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB,
+                                    Cfg::BK, Cfg::BNC, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!mapA || !mapB) return EMU_STATUS_NOT_SUPPORTED;
     int tma_store = beta == 0.0f && aligned16(C) && ldc % 4 == 0 && (!c_b || strideC % 4 == 0) &&
                     (unsigned long long)strideC * 4 < (1ull << 40);
     if (tma_store) {
@@ -417,7 +421,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     p.unit_tiles = ASTAT ? p.tiles_n : 1;
     if (ASTAT && p.num_k_stages > Cfg::ASLOTS) return EMU_STATUS_NOT_SUPPORTED;   // dispatch guarantees it
     const long long clusters = std::min<long long>(p.num_units, sms / 2);
-    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT>
+    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>
         <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
@@ -449,13 +453,15 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
                             const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                             long long strideC, int batch, emu_split_mode mode, void* stream,
                             unsigned int* d_range_flag, int kblock, unsigned int flags, void* range_ws,
-                            size_t range_ws_bytes)
+                            size_t range_ws_bytes, bool ta = false, bool tb = false)
 {
     g_last_launches = 0;
     // ---- synchronous validation (C untouched on error) ----
     if (m < 0 || n < 0 || k < 0 || batch < 0) return EMU_STATUS_INVALID_VALUE;
     if (mode != EMU_SPLIT_FP16 && mode != EMU_SPLIT_TF32) return EMU_STATUS_INVALID_VALUE;
-    if (lda < std::max(1, m) || ldb < std::max(1, k) || ldc < std::max(1, m)) return EMU_STATUS_INVALID_VALUE;
+    if (lda < std::max(1, ta ? k : m) || ldb < std::max(1, tb ? n : k) || ldc < std::max(1, m))
+        return EMU_STATUS_INVALID_VALUE;
+    if (range_ws != nullptr && (ta || tb)) return EMU_STATUS_NOT_SUPPORTED;
     if (strideA < 0 || strideB < 0 || strideC < 0) return EMU_STATUS_INVALID_VALUE;
     if (kblock < 0 || (kblock > 0 && (kblock % 32 != 0 || kblock > 4096))) return EMU_STATUS_INVALID_VALUE;
     if (flags & ~EMU_FLAG_NO_CORRECTION) return EMU_STATUS_INVALID_VALUE;
@@ -519,7 +525,8 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     // A-in-TMEM pair kernel (fewest shared-memory bytes per MMA) for every problem
     // with more than one 128-row block; the SMEM-operand pair kernel stays selectable
     // (EMU_KERNEL=pair) for comparison.
-    const bool ts = !ldg && (range || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
+    if ((ta || tb) && !tma_ok) return EMU_STATUS_NOT_SUPPORTED;   // transposed operands: TS kernel only
+    const bool ts = !ldg && (range || ta || tb || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     // tile width of the TS kernel (profiles/r01_summary.md): 128 with one accumulator
     // buffer whose D_corr and D_hi drains overlap the other part's MMAs (SPLITC); the
@@ -555,6 +562,35 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
                                                                  strideB, beta, C, ldc, strideC, batch, s,             \
                                                                  d_range_flag, kblock, flags, row_max, col_max); break; }       \
     } while (0)
+#define EMU_RUN_TT(MODE_, RANGE_, TA_, TB_)                                                                            \
+    do {                                                                                                               \
+        if (ts_as)                                                                                                     \
+            rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, true, TA_, TB_>(                                           \
+                dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, s,           \
+                d_range_flag, kblock, flags, nullptr, nullptr);                                                        \
+        else                                                                                                           \
+            rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, false, TA_, TB_>(                                          \
+                dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, s,           \
+                d_range_flag, kblock, flags, nullptr, nullptr);                                                        \
+    } while (0)
+#define EMU_RUN_T3(MODE_, RANGE_)                                                                                      \
+    do {                                                                                                               \
+        if (ta && tb) EMU_RUN_TT(MODE_, RANGE_, true, true);                                                           \
+        else if (ta) EMU_RUN_TT(MODE_, RANGE_, true, false);                                                           \
+        else EMU_RUN_TT(MODE_, RANGE_, false, true);                                                                   \
+    } while (0)
+    if (ta || tb) {   // op(A) / op(B) transposed (NEXT row 2): split-commit TS kernel, 128-wide tiles
+        emu_status rs;
+        if (mode == EMU_SPLIT_FP16) {
+            if (d_range_flag) EMU_RUN_T3(0, true);
+            else EMU_RUN_T3(0, false);
+        } else {
+            EMU_RUN_T3(1, false);
+        }
+        return rs;
+    }
+#undef EMU_RUN_T3
+#undef EMU_RUN_TT
     if (ts) {
         emu_status rs;
         if (mode == EMU_SPLIT_FP16) {
@@ -606,6 +642,24 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_ex(int m, in
 {
     return gemm_impl(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, mode, stream,
                      d_range_flag, kblock, flags, nullptr, 0);
+}
+
+__attribute__((visibility("default"))) emu_status emu_sgemm_batched_t(char transa, char transb, int m, int n, int k, float alpha,
+                               const float* A, int lda, long long strideA, const float* B, int ldb,
+                               long long strideB, float beta, float* C, int ldc, long long strideC,
+                               int batch, emu_split_mode mode, void* stream, unsigned int* d_range_flag,
+                               int kblock, unsigned int flags)
+{
+    auto op = [](char t, bool& tr) {
+        if (t == 'N' || t == 'n') { tr = false; return true; }
+        if (t == 'T' || t == 't' || t == 'C' || t == 'c') { tr = true; return true; }
+        return false;
+    };
+    bool ta = false, tb = false;
+    g_last_launches = 0;
+    if (!op(transa, ta) || !op(transb, tb)) return EMU_STATUS_INVALID_VALUE;
+    return gemm_impl(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, mode, stream,
+                     d_range_flag, kblock, flags, nullptr, 0, ta, tb);
 }
 
 __attribute__((visibility("default"))) size_t emu_range_workspace_size(int m, int n, int batch)

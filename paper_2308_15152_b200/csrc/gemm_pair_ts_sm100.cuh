@@ -107,7 +107,9 @@ __device__ __forceinline__ void ts_unit_tile(const GemmParams& p, long long u, i
     }
 }
 
-template <int MODE, bool RANGE, int BN, bool SPLITC_, bool ASTAT_>
+// TA / TB: op(A) = A^T (A stored k x m, k contiguous) / op(B) = B^T (B stored n x k):
+// only the TMA boxes and the splitters' shared-memory reads change (NEXT row 2)
+template <int MODE, bool RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, SPLITC_, ASTAT_>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
@@ -187,11 +189,20 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                             uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                             TRACE_AT(0, 1, ks);
                             ptx::mbar_arrive_expect_tx(&f32_full[s], loadA ? Cfg::F32_STAGE : Cfg::B32_BYTES);
-                            if (loadA)
-                                ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM,
-                                                        ks * Cfg::BK, ab);
-                            ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
-                                                    nt * Cfg::BN + rank * Cfg::BNC, bb);
+                            if (loadA) {
+                                if (TA)   // [128 m][32 k], SWIZZLE_128B rows
+                                    ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], ks * Cfg::BK,
+                                                            mt * 256 + rank * Cfg::BM, ab);
+                                else      // [32 k][128 m]
+                                    ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM,
+                                                            ks * Cfg::BK, ab);
+                            }
+                            if (TB)       // [32 k][BN/2 n]
+                                ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s],
+                                                        nt * Cfg::BN + rank * Cfg::BNC, ks * Cfg::BK, bb);
+                            else          // [BN/2 n][32 k], SWIZZLE_128B rows
+                                ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
+                                                        nt * Cfg::BN + rank * Cfg::BNC, bb);
                             if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                         }
                     }
@@ -382,12 +393,29 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     // ---- load phase: A(m, KS kq .. +KS-1) (a warp reads 32 consecutive m per k),
                     //      B(8 quarter .. +7, n): FP32 16-byte chunks 2 quarter, 2 quarter + 1 of row n
                     float av[Cfg::KS];
-                    if (doA) {
+                    if (doA && TA) {
+                        // row m holds 32 k (128 bytes, 16-byte chunks XOR-swizzled by m & 7)
+                        const uint8_t* ra = reinterpret_cast<const uint8_t*>(fa) + m * 128;
+#pragma unroll
+                        for (int cc = 0; cc < Cfg::KS / 4; ++cc) {
+                            const float4 v = *reinterpret_cast<const float4*>(
+                                ra + (((kq * (Cfg::KS / 4) + cc) ^ (m & 7)) << 4));
+                            av[4 * cc] = v.x; av[4 * cc + 1] = v.y; av[4 * cc + 2] = v.z; av[4 * cc + 3] = v.w;
+                        }
+                    } else if (doA) {
 #pragma unroll
                         for (int jj = 0; jj < Cfg::KS; ++jj) av[jj] = fa[(kq * Cfg::KS + jj) * Cfg::BM + m];
                     }
                     float4 vb[2];
-                    if (has_b) {
+                    if (has_b && TB) {
+                        // k-row of BN/2 columns: a warp reads 32 consecutive n per k
+                        const float* fbt = reinterpret_cast<const float*>(fb);
+                        float x[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) x[i] = fbt[(quarter * 8 + i) * Cfg::BNC + n];
+                        vb[0] = make_float4(x[0], x[1], x[2], x[3]);
+                        vb[1] = make_float4(x[4], x[5], x[6], x[7]);
+                    } else if (has_b) {
 #pragma unroll
                         for (int c = 0; c < 2; ++c)
                             vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));

@@ -116,3 +116,24 @@ def test_range_entry_validation(emu):
     empty = list(args)
     empty[14] = 0                                                             # batch = 0: quick return
     assert L.emu_sgemm_batched_range(*empty, 4096, 0, None, 0, 0) == 0
+
+
+def test_transpose_entry_validation(emu):
+    """emu_sgemm_batched_t: trans characters and the transposed leading-dimension
+    rules are checked before any CUDA call (NEXT row 2)."""
+    L = emu.lib
+    base = dict(m=8, n=16, k=32, alpha=1.0, A=16, lda=8, sA=0, B=16, ldb=32, sB=0, beta=0.0, C=16, ldc=8,
+                sC=0, batch=1, mode=0)
+
+    def call(ta, tb, **kw):
+        a = dict(base)
+        a.update(kw)
+        return L.emu_sgemm_batched_t(ta, tb, a["m"], a["n"], a["k"], a["alpha"], a["A"], a["lda"], a["sA"],
+                                     a["B"], a["ldb"], a["sB"], a["beta"], a["C"], a["ldc"], a["sC"],
+                                     a["batch"], a["mode"], None, None, 0, 0)
+    assert call(b"X", b"N") == 1
+    assert call(b"N", b"Q") == 1
+    assert call(b"T", b"N", lda=8) == 1        # A stored k x m: lda >= k = 32
+    assert call(b"N", b"T", ldb=8) == 1        # B stored n x k: ldb >= n = 16
+    assert call(b"t", b"n", lda=32, batch=0) == 0   # valid, quick return
+    assert call(b"C", b"c", lda=32, ldb=16, batch=0) == 0
