@@ -13,7 +13,11 @@ HEADER = os.path.join(ROOT, "include", "emu_sgemm.h")
 
 @pytest.fixture(scope="module")
 def emu():
-    from paper_2308_15152_b200 import build
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_emu_build", os.path.join(ROOT, "paper_2308_15152_b200", "build.py"))
+    build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(build)  # by path: the package import needs the .so first
     build.build()
     import paper_2308_15152_b200 as emu
     return emu
