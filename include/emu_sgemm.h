@@ -62,6 +62,8 @@ typedef enum {
 /* Flags for emu_sgemm_batched_ex. */
 #define EMU_FLAG_NO_CORRECTION 1u  /* policy "error correction off": drop both
                                       correction products; a negative control only */
+#define EMU_FLAG_SIMT 2u           /* emu_tcec_* only: the device API's "simt" backend,
+                                      the same three products on CUDA cores, for evaluation */
 
 /*
  * emu_sgemm_batched -- C_b = alpha * A_b B_b + beta * C_b for b in [0, batch).
@@ -186,6 +188,54 @@ emu_status emu_sgemm_batched_host(int m, int n, int k, float alpha,
  */
 emu_status emu_split(const float* x, long long count, emu_split_mode mode,
                      void* hi, void* lo, void* stream);
+
+/*
+ * Device-level API users (include/emu_tcec.cuh).  Each
+ * entry is ONE kernel written against the in-kernel tile API emu::tcec::tile
+ * (the B200 analog of WMMAe-TCEC): 128 x 64 output blocks per
+ * 128-thread CTA (128 x 32 with EMU_FLAG_SIMT), k in stages of 64 (FP16) / 32
+ * (TF32) split on load, three tcgen05 products per stage, combine every 64 k.
+ * flags: EMU_FLAG_NO_CORRECTION (policy without_ec, P1 only) and/or
+ * EMU_FLAG_SIMT (policy simt: the products on CUDA cores).  Column-major,
+ * device pointers owned by the caller, asynchronous on `stream`; any alignment.
+ * Errors as emu_sgemm_batched; unknown flag bits -> EMU_STATUS_INVALID_VALUE;
+ * more than 65535 column blocks -> EMU_STATUS_NOT_SUPPORTED.
+ *
+ * emu_tcec_gemm_batched: C_b = alpha A_b B_b + beta C_b, arguments as
+ *   emu_sgemm_batched_ex (kblock: combine interval, 0 = 64, else a multiple of
+ *   the stage k (64 FP16 / 32 TF32), at most 4096).  The paper's "Code 1 with the
+ *   namespace swapped".
+ * emu_tcec_householder_batched: C_b = H_b X_b, H_b = I_m - 2 v_b v_b^T
+ *   (Eq. householder, read as v v^T for a unit column v, R#23),
+ *   H(i, p) = RN(RN(RN(v_i v_p) * -2) + [i == p]) generated inside the kernel by
+ *   the foreach_ij analog (Code 4); H is never stored.  v_b =
+ *   V + b*strideV (m floats); X_b m x n (ldx >= m); C_b m x n (ldc >= m).
+ * emu_tcec_givens_batched: C_b = G(i, j, theta_b) X_b (R#24): G = I_m
+ *   except G(i,i) = G(j,j) = c_b, G(i,j) = -s_b, G(j,i) = s_b with (c_b, s_b) =
+ *   (CS[2b], CS[2b+1]); built with the map analog.  0 <= i, j < m,
+ *   i != j, else EMU_STATUS_INVALID_VALUE.
+ * emu_tcec_scan: inclusive prefix sums of `count` arrays of n floats, array c at
+ *   X + c*ldx, result at Y + c*ldy: y = L x, L(i, p) = [p <= i] (the transpose of
+ *   the paper's U, Eqs. scan-mat / u-rule, R#25), L generated by rule.
+ */
+emu_status emu_tcec_gemm_batched(int m, int n, int k, float alpha,
+                                 const float* A, int lda, long long strideA,
+                                 const float* B, int ldb, long long strideB,
+                                 float beta, float* C, int ldc, long long strideC,
+                                 int batch, emu_split_mode mode, void* stream,
+                                 int kblock, unsigned int flags);
+emu_status emu_tcec_householder_batched(int m, int n, const float* V, long long strideV,
+                                        const float* X, int ldx, long long strideX,
+                                        float* C, int ldc, long long strideC,
+                                        int batch, emu_split_mode mode, void* stream,
+                                        unsigned int flags);
+emu_status emu_tcec_givens_batched(int m, int n, int i, int j, const float* CS,
+                                   const float* X, int ldx, long long strideX,
+                                   float* C, int ldc, long long strideC,
+                                   int batch, emu_split_mode mode, void* stream,
+                                   unsigned int flags);
+emu_status emu_tcec_scan(int n, int count, const float* X, int ldx, float* Y, int ldy,
+                         emu_split_mode mode, void* stream, unsigned int flags);
 
 /* Number of kernel launches the last successful call on this host thread
  * issued (0 for a quick return without a scale kernel); for launch accounting. */

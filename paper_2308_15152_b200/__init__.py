@@ -16,6 +16,8 @@ __all__ = [
     "EMU_SPLIT_FP16", "EMU_SPLIT_TF32", "EMU_FLAG_NO_CORRECTION", "EmuError", "lib", "LIB_PATH",
     "emu_sgemm", "emu_sgemm_batched", "emu_sgemm_batched_ex", "emu_sgemm_batched_host",
     "emu_split", "emu_status_string", "emu_version", "emu_last_launch_count", "mode_of",
+    "EMU_FLAG_SIMT", "emu_tcec_gemm_batched", "emu_tcec_householder_batched", "emu_tcec_givens_batched",
+    "emu_tcec_scan",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libemusgemm.so")
@@ -23,6 +25,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libemusgemm
 EMU_SPLIT_FP16 = 0
 EMU_SPLIT_TF32 = 1
 EMU_FLAG_NO_CORRECTION = 1
+EMU_FLAG_SIMT = 2
 STATUS = {0: "SUCCESS", 1: "INVALID_VALUE", 2: "NOT_SUPPORTED", 3: "ARCH_MISMATCH",
           4: "LAUNCH_FAILED", 5: "CUDA_ERROR"}
 
@@ -61,6 +64,14 @@ lib.emu_sgemm.argtypes = [_i, _i, _i, _f, _p, _i, _p, _i, _f, _p, _i, _i, _p]
 lib.emu_sgemm.restype = _i
 lib.emu_split.argtypes = [_p, _ll, _i, _p, _p, _p]
 lib.emu_split.restype = _i
+lib.emu_tcec_gemm_batched.argtypes = _GEMM_ARGS + [_i, _u]
+lib.emu_tcec_gemm_batched.restype = _i
+lib.emu_tcec_householder_batched.argtypes = [_i, _i, _p, _ll, _p, _i, _ll, _p, _i, _ll, _i, _i, _p, _u]
+lib.emu_tcec_householder_batched.restype = _i
+lib.emu_tcec_givens_batched.argtypes = [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _i, _i, _p, _u]
+lib.emu_tcec_givens_batched.restype = _i
+lib.emu_tcec_scan.argtypes = [_i, _i, _p, _i, _p, _i, _i, _p, _u]
+lib.emu_tcec_scan.restype = _i
 lib.emu_status_string.argtypes = [_i]
 lib.emu_status_string.restype = ctypes.c_char_p
 lib.emu_version.argtypes = []
@@ -155,6 +166,33 @@ def emu_sgemm(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, mode, stream=None):
 
 def emu_split(x, count, mode, hi, lo, stream=None):
     _check(lib.emu_split(_ptr(x), count, mode_of(mode), _ptr(hi), _ptr(lo), _stream(stream)), "emu_split")
+
+
+def emu_tcec_gemm_batched(m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+                          batch, mode, stream=None, kblock=0, flags=0):
+    _check(lib.emu_tcec_gemm_batched(m, n, k, alpha, _ptr(A), lda, strideA, _ptr(B), ldb, strideB,
+                                     beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream),
+                                     kblock, flags),
+           "emu_tcec_gemm_batched")
+
+
+def emu_tcec_householder_batched(m, n, V, strideV, X, ldx, strideX, C, ldc, strideC, batch, mode,
+                                 stream=None, flags=0):
+    _check(lib.emu_tcec_householder_batched(m, n, _ptr(V), strideV, _ptr(X), ldx, strideX, _ptr(C), ldc,
+                                            strideC, batch, mode_of(mode), _stream(stream), flags),
+           "emu_tcec_householder_batched")
+
+
+def emu_tcec_givens_batched(m, n, i, j, CS, X, ldx, strideX, C, ldc, strideC, batch, mode, stream=None,
+                            flags=0):
+    _check(lib.emu_tcec_givens_batched(m, n, i, j, _ptr(CS), _ptr(X), ldx, strideX, _ptr(C), ldc, strideC,
+                                       batch, mode_of(mode), _stream(stream), flags),
+           "emu_tcec_givens_batched")
+
+
+def emu_tcec_scan(n, count, X, ldx, Y, ldy, mode, stream=None, flags=0):
+    _check(lib.emu_tcec_scan(n, count, _ptr(X), ldx, _ptr(Y), ldy, mode_of(mode), _stream(stream), flags),
+           "emu_tcec_scan")
 
 
 def emu_status_string(status: int) -> str:

@@ -12,7 +12,7 @@ SRC_DIR = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libemusgemm.so")
 SOURCES = [os.path.join(SRC_DIR, "api.cu")]
 DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in os.listdir(SRC_DIR) if f.endswith(".cuh")] + \
-    [os.path.join(ROOT, "include", "emu_sgemm.h")]
+    [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

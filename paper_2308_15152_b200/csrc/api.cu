@@ -855,3 +855,6 @@ __attribute__((visibility("default"))) int emu_trace_read(long long* host, unsig
 #endif
 
 }  // extern "C"
+
+// device-level API users (include/emu_tcec.cuh): tcec GEMM, Householder, Givens, scan
+#include "tcec_api.cuh"

@@ -141,3 +141,28 @@ def test_transpose_entry_validation(emu):
     assert call(b"N", b"T", ldb=8) == 1        # B stored n x k: ldb >= n = 16
     assert call(b"t", b"n", lda=32, batch=0) == 0   # valid, quick return
     assert call(b"C", b"c", lda=32, ldb=16, batch=0) == 0
+
+
+def test_tcec_entries_validation(emu):
+    """device-API users (NEXT rows 2 and 4): argument checks run before any CUDA call"""
+    L = emu.lib
+    g = [8, 8, 8, 1.0, 16, 8, 0, 16, 8, 0, 0.0, 16, 8, 0, 1, 0, None]
+    assert L.emu_tcec_gemm_batched(*g, 0, 4) == 1            # unknown flag bit
+    assert L.emu_tcec_gemm_batched(*g, 32, 0) == 1           # FP16 kblock below the 64-k stage
+    assert L.emu_tcec_gemm_batched(*g, 96, 0) == 1           # not a multiple of 64
+    assert L.emu_tcec_gemm_batched(*g, 0, 8) == 1
+    bad = list(g)
+    bad[5] = 7                                                 # lda < m
+    assert L.emu_tcec_gemm_batched(*bad, 0, 0) == 1
+    empty = list(g)
+    empty[14] = 0
+    assert L.emu_tcec_gemm_batched(*empty, 0, 3) == 0        # batch 0: quick return, flags valid
+    # Householder / Givens / scan
+    assert L.emu_tcec_householder_batched(8, 8, 16, 8, 16, 7, 64, 16, 8, 64, 1, 0, None, 0) == 1   # ldx < m
+    assert L.emu_tcec_householder_batched(8, 8, None, 8, 16, 8, 64, 16, 8, 64, 1, 0, None, 0) == 1
+    assert L.emu_tcec_givens_batched(8, 8, 3, 3, 16, 16, 8, 64, 16, 8, 64, 1, 0, None, 0) == 1      # i == j
+    assert L.emu_tcec_givens_batched(8, 8, 3, 8, 16, 16, 8, 64, 16, 8, 64, 1, 0, None, 0) == 1      # j >= m
+    assert L.emu_tcec_givens_batched(8, 8, 1, 2, 16, 16, 8, 64, 16, 8, 64, 0, 0, None, 0) == 0      # batch 0
+    assert L.emu_tcec_scan(8, 4, 16, 7, 16, 8, 0, None, 0) == 1                                    # ldx < n
+    assert L.emu_tcec_scan(8, 4, 16, 8, 16, 8, 3, None, 0) == 1                                    # mode
+    assert L.emu_tcec_scan(0, 4, None, 1, None, 1, 0, None, 0) == 0                                # n = 0

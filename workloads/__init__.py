@@ -20,7 +20,7 @@ import numpy as np
 
 __all__ = [
     "rng", "uniform", "log_uniform", "small_int", "colmajor", "math_view",
-    "Config", "CONFIGS", "make_operands",
+    "Config", "CONFIGS", "make_operands", "unit_vectors", "rotations",
 ]
 
 
@@ -121,3 +121,17 @@ def make_operands(batch: int, m: int, n: int, k: int, seed: int,
         A[b, :, :m] = _draw((k, m), (seed * 1000003 + g) * 2 + 0, dist)
         B[b, :, :k] = _draw((n, k), (seed * 1000003 + g) * 2 + 1, dist)
     return A, B
+
+
+def unit_vectors(batch: int, m: int, seed: int) -> np.ndarray:
+    """(batch, m) float32 Householder vectors: uniform[-1,1] directions scaled
+    to unit 2-norm in float64, rounded once to float32 (so ||v|| = 1 + O(u))."""
+    x = uniform((batch, m), seed).astype(np.float64)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    return x.astype(np.float32)
+
+
+def rotations(batch: int, seed: int) -> np.ndarray:
+    """(batch, 2) float32 (c, s) = (cos t, sin t), t uniform in [0, 2 pi)."""
+    t = rng(seed).uniform(0.0, 2.0 * np.pi, size=batch)
+    return np.stack([np.cos(t), np.sin(t)], axis=1).astype(np.float32)
