@@ -233,6 +233,75 @@ def _config(cfg, mode, world):
                   4 * (cfg.m * cfg.k + cfg.k * cfg.n + cfg.m * cfg.n) * cfg.batch > 126e6 else "small"}
 
 
+def run_c3_sharded(args, rank, world, local):
+    """c3 over N GPUs (SURVEY §8(f) NEXT 3, strong scaling): one 16384^3 GEMM, B and
+    C in column blocks, A replicated; each step = every rank's block GEMM with the
+    all-gather of C fused into its epilogue (emu_sgemm_multicast into the peers'
+    symmetric-memory buffers) + a device barrier.  Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2308_15152_b200 as emu
+    from paper_2308_15152_b200.sharded import ShardedGemm
+    cfg = workloads.CONFIGS["c3"]
+    m, n, k, mode = cfg.m, cfg.n, cfg.k, args.mode
+    A_h, B_h = workloads.make_operands(1, m, n, k, cfg.seed)
+    g = ShardedGemm(m, n, k)
+    dA = torch.from_numpy(A_h[0]).cuda()
+    dB = torch.from_numpy(np.ascontiguousarray(B_h[0, g.n0:g.n1])).cuda()
+    stream = torch.cuda.current_stream()
+    launches = 0
+
+    def step():
+        nonlocal launches
+        g(dA, dB, mode, stream)
+        launches += emu.emu_last_launch_count()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms_max = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
+    ms_per_step = ms_max / args.steps
+    value = 2.0 * m * n * k / (ms_per_step / 1e3) / 1e12
+    # every rank's gathered C, sampled against FP64 (outside the timed region)
+    gg = workloads.rng(5 + rank)
+    ii, jj = gg.integers(0, m, 256), gg.integers(0, n, 256)
+    got = g.C[torch.from_numpy(jj), torch.from_numpy(ii)].cpu().numpy().astype(np.float64)
+    R = np.array([np.dot(A_h[0, :, i].astype(np.float64), B_h[0, j, :].astype(np.float64)) for i, j in zip(ii, jj)])
+    err = max_over_ranks(float(np.linalg.norm(got - R) / np.linalg.norm(R)), device="cuda")
+    peaks = _peaks()
+    tc_peak_sus = peaks["bf16_tflops_sustained"] * (1.0 if mode == "fp16" else 0.5)
+    achieved = 6.0 * m * (g.n1 - g.n0) * k / (ms_per_step / 1e3) / 1e12   # this rank's tensor work
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"c3: {cfg.note}; {mode} split; n-sharded over {world} GPUs",
+                   "m": m, "n": n, "k": k, "split": mode, "parallelism": f"column-shard x{world}",
+                   "exchange": g.exchange, "l2": "no flush: inputs per step exceed the 126 MB L2"},
+        "rel_frobenius_vs_fp64": err, "accuracy_sample": "256 sampled outputs of every rank's gathered C",
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak_sus, "unit": "TFLOP/s",
+                     "frac": achieved / tc_peak_sus, "traffic": None,
+                     "note": "rank 0's block GEMM incl. the fused all-gather and barrier"},
+        "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk.summary(),
+        "paper_context": PAPER_A100,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = _args()
     if args.impl == "reference":
@@ -249,6 +318,9 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == "c3" and world > 1:
+        run_c3_sharded(args, rank, world, local)
+        return
     cfg = workloads.CONFIGS[args.config]
     m, n, k, batch = cfg.m, cfg.n, cfg.k, cfg.batch
     mode = args.mode

@@ -190,6 +190,25 @@ emu_status emu_split(const float* x, long long count, emu_split_mode mode,
                      void* hi, void* lo, void* stream);
 
 /*
+ * emu_sgemm_multicast -- one GEMM C = alpha A B (beta = 0: C is never read) whose
+ * result is stored to num_dst (1..8) destinations C_dst[0..num_dst-1], each m x n
+ * with leading dimension ldc.  C_dst is a HOST array of
+ * device pointers; a pointer may be a peer GPU's memory mapped into this process
+ * (CUDA IPC / symmetric memory over NVLink): then the kernel's epilogue writes
+ * every finished tile to every peer while later tiles are still computing -- the
+ * all-gather of an n-sharded GEMM fused into the GEMM (rank r passes its column
+ * block B_r and C_dst[q] = C_q + n0_r*ldc).  Same method and arithmetic as
+ * emu_sgemm (bit-identical per element).  Requires the TMA domain (A, B 16-byte
+ * aligned, lda, ldb multiples of 4) else EMU_STATUS_NOT_SUPPORTED; num_dst out of
+ * range or a NULL destination -> EMU_STATUS_INVALID_VALUE; other errors as
+ * emu_sgemm_batched_ex.  Destinations must not overlap each other, A or B.
+ */
+emu_status emu_sgemm_multicast(int m, int n, int k, float alpha,
+                               const float* A, int lda, const float* B, int ldb,
+                               float* const* C_dst, int num_dst, int ldc,
+                               emu_split_mode mode, void* stream, int kblock, unsigned int flags);
+
+/*
  * Device-level API users (include/emu_tcec.cuh).  Each
  * entry is ONE kernel written against the in-kernel tile API emu::tcec::tile
  * (the B200 analog of WMMAe-TCEC): 128 x 64 output blocks per

@@ -17,7 +17,7 @@ __all__ = [
     "emu_sgemm", "emu_sgemm_batched", "emu_sgemm_batched_ex", "emu_sgemm_batched_host",
     "emu_split", "emu_status_string", "emu_version", "emu_last_launch_count", "mode_of",
     "EMU_FLAG_SIMT", "emu_tcec_gemm_batched", "emu_tcec_householder_batched", "emu_tcec_givens_batched",
-    "emu_tcec_scan",
+    "emu_tcec_scan", "emu_sgemm_multicast",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libemusgemm.so")
@@ -72,6 +72,8 @@ lib.emu_tcec_givens_batched.argtypes = [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i,
 lib.emu_tcec_givens_batched.restype = _i
 lib.emu_tcec_scan.argtypes = [_i, _i, _p, _i, _p, _i, _i, _p, _u]
 lib.emu_tcec_scan.restype = _i
+lib.emu_sgemm_multicast.argtypes = [_i, _i, _i, _f, _p, _i, _p, _i, ctypes.POINTER(_p), _i, _i, _i, _p, _i, _u]
+lib.emu_sgemm_multicast.restype = _i
 lib.emu_status_string.argtypes = [_i]
 lib.emu_status_string.restype = ctypes.c_char_p
 lib.emu_version.argtypes = []
@@ -193,6 +195,14 @@ def emu_tcec_givens_batched(m, n, i, j, CS, X, ldx, strideX, C, ldc, strideC, ba
 def emu_tcec_scan(n, count, X, ldx, Y, ldy, mode, stream=None, flags=0):
     _check(lib.emu_tcec_scan(n, count, _ptr(X), ldx, _ptr(Y), ldy, mode_of(mode), _stream(stream), flags),
            "emu_tcec_scan")
+
+
+def emu_sgemm_multicast(m, n, k, alpha, A, lda, B, ldb, C_dst, ldc, mode, stream=None, kblock=0, flags=0):
+    """C_dst: sequence of device buffers / addresses (1..8), each receiving C = alpha A B."""
+    arr = (_p * len(C_dst))(*[_ptr(c) for c in C_dst])
+    _check(lib.emu_sgemm_multicast(m, n, k, alpha, _ptr(A), lda, _ptr(B), ldb, arr, len(C_dst), ldc,
+                                   mode_of(mode), _stream(stream), kblock, flags),
+           "emu_sgemm_multicast")
 
 
 def emu_status_string(status: int) -> str:

@@ -22,6 +22,14 @@ namespace {
 
 thread_local int g_last_launches = 0;
 
+// extra result destinations of the emu_sgemm_multicast call in progress on this
+// host thread (nullptr otherwise); read by the TS-kernel launcher
+struct MultiDst {
+    int n;
+    float* d[8];
+};
+thread_local const MultiDst* g_mdst = nullptr;
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -387,6 +395,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     if (!mapA || !mapB) return EMU_STATUS_NOT_SUPPORTED;
     int tma_store = beta == 0.0f && aligned16(C) && ldc % 4 == 0 && (!c_b || strideC % 4 == 0) &&
                     (unsigned long long)strideC * 4 < (1ull << 40);
+    if (g_mdst && g_mdst->n > 1) tma_store = 0;   // multicast: st.global to every destination
     if (tma_store) {
         const uint64_t sC = c_b ? (uint64_t)strideC : (((uint64_t)ldc * (uint64_t)n + 3) & ~uint64_t(3));
         // one 32-row x ECOLS block per combine warp (each warp stores its own columns)
@@ -417,6 +426,10 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     p.row_max = row_max;
     p.col_max = col_max;
+    if (g_mdst) {
+        p.num_dst = g_mdst->n;
+        for (int d = 0; d < g_mdst->n; ++d) p.dst[d] = g_mdst->d[d];
+    }
     p.num_units = ASTAT ? (long long)p.tiles_m * batch : p.num_tiles;
     p.unit_tiles = ASTAT ? p.tiles_n : 1;
     if (ASTAT && p.num_k_stages > Cfg::ASLOTS) return EMU_STATUS_NOT_SUPPORTED;   // dispatch guarantees it
@@ -526,7 +539,8 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     // with more than one 128-row block; the SMEM-operand pair kernel stays selectable
     // (EMU_KERNEL=pair) for comparison.
     if ((ta || tb) && !tma_ok) return EMU_STATUS_NOT_SUPPORTED;   // transposed operands: TS kernel only
-    const bool ts = !ldg && (range || ta || tb || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
+    if (g_mdst && !tma_ok) return EMU_STATUS_NOT_SUPPORTED;   // multicast: TS kernel only
+    const bool ts = !ldg && (range || ta || tb || g_mdst || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     // tile width of the TS kernel (profiles/r01_summary.md): 128 with one accumulator
     // buffer whose D_corr and D_hi drains overlap the other part's MMAs (SPLITC); the
@@ -853,6 +867,42 @@ __attribute__((visibility("default"))) int emu_trace_read(long long* host, unsig
     return emu::TRACE_ROLES;
 }
 #endif
+
+}  // extern "C"
+
+extern "C" {
+
+// one GEMM, result stored to several destinations (NEXT row 3: the epilogue of an
+// n-sharded GEMM with its all-gather fused in)
+__attribute__((visibility("default"))) emu_status emu_sgemm_multicast(
+    int m, int n, int k, float alpha, const float* A, int lda, const float* B, int ldb, float* const* C_dst,
+    int num_dst, int ldc, emu_split_mode mode, void* stream, int kblock, unsigned int flags)
+{
+    g_last_launches = 0;
+    if (C_dst == nullptr || num_dst < 1 || num_dst > 8) return EMU_STATUS_INVALID_VALUE;
+    MultiDst md;
+    md.n = num_dst;
+    for (int d = 0; d < num_dst; ++d) {
+        if (C_dst[d] == nullptr) return EMU_STATUS_INVALID_VALUE;
+        md.d[d] = C_dst[d];
+    }
+    struct Guard {
+        explicit Guard(const MultiDst* p) { g_mdst = p; }
+        ~Guard() { g_mdst = nullptr; }
+    } guard(&md);
+    // k == 0 / alpha == 0 quick path writes C_dst[0] only: route every destination through it
+    if (k == 0 || alpha == 0.0f) {
+        for (int d = 0; d < num_dst; ++d) {
+            const emu_status st = gemm_impl(m, n, k, alpha, A, lda, 0, B, ldb, 0, 0.0f, C_dst[d], ldc, 0, 1, mode,
+                                            stream, nullptr, kblock, flags, nullptr, 0);
+            if (st != EMU_STATUS_SUCCESS) return st;
+        }
+        if (m > 0 && n > 0) g_last_launches = num_dst;
+        return EMU_STATUS_SUCCESS;
+    }
+    return gemm_impl(m, n, k, alpha, A, lda, 0, B, ldb, 0, 0.0f, C_dst[0], ldc, 0, 1, mode, stream, nullptr, kblock,
+                     flags, nullptr, 0);
+}
 
 }  // extern "C"
 

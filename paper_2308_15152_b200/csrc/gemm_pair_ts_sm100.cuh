@@ -663,6 +663,14 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll
                             for (int jj = 0; jj < HALF; ++jj)
                                 if (col0 + jj < p.n) cp[(long long)jj * p.ldc] = fmaf(p.alpha, creg[jj], 0.0f);
+                            // fused all-gather (NEXT row 3): the same tile to every other
+                            // destination -- peer C buffers over NVLink on a multi-GPU run
+                            for (int d = 1; d < p.num_dst; ++d) {
+                                float* dp = p.dst[d] + r + (long long)col0 * p.ldc;
+#pragma unroll
+                                for (int jj = 0; jj < HALF; ++jj)
+                                    if (col0 + jj < p.n) dp[(long long)jj * p.ldc] = fmaf(p.alpha, creg[jj], 0.0f);
+                            }
                         }
                     }
                 }

@@ -119,6 +119,10 @@ struct GemmParams {
     const float* A;
     const float* B;
     long long lda, ldb, strideA, strideB;   // elements; stride 0 = shared operand
+    // TS kernel, single problem (emu_sgemm_multicast): the result is also stored to
+    // dst[1 .. num_dst-1] (same ldc; peers' buffers for a fused all-gather); 0/1 = C only
+    int num_dst;
+    float* dst[8];
 };
 
 // range-safe mode: exponent e = clamp(ilogb(max) - 14, -125, 125) of a row / column from
