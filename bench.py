@@ -65,7 +65,7 @@ def _args():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="fp16", choices=["fp16", "tf32"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -175,7 +175,9 @@ def _cpu_baseline(cfg, mode, A_host, B_host, budget_s=15.0):
         jj = g.integers(0, n, nent)
         bb = np.zeros(nent, dtype=np.int64)
         t0 = time.perf_counter()
-        oracle.emu_gemm_entries(mode, A_host, B_host, m, n, k, bb, ii, jj)
+        entries = oracle.emu_gemm_range_entries if (cfg.dist == "logu30" and mode == "fp16") \
+            else oracle.emu_gemm_entries
+        entries(mode, A_host, B_host, m, n, k, bb, ii, jj)
         dt = time.perf_counter() - t0
         flops = 2.0 * k * nent
         sample = f"{nent} sampled outputs of the {m}x{n}x{k} GEMM (full k each)"
@@ -193,17 +195,19 @@ def run_reference(args):
     m, n, k = cfg.m, cfg.n, cfg.k
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if cfg.batch > 1:
-        A, B = workloads.make_operands(1, m, n, k, cfg.seed)
+        A, B = workloads.make_operands(1, m, n, k, cfg.seed, dist=cfg.dist)
         step = lambda: oracle.emu_gemm(args.mode, A, B, m, n, k)   # noqa: E731
         flops = 2.0 * m * n * k
         sample = f"each step: 1 of the {cfg.batch} problems ({m}x{n}x{k}) of the workload"
     else:
-        A, B = workloads.make_operands(1, m, n, k, cfg.seed)
+        A, B = workloads.make_operands(1, m, n, k, cfg.seed, dist=cfg.dist)
+        emu_entries = oracle.emu_gemm_range_entries if (cfg.dist == "logu30" and args.mode == "fp16") \
+            else oracle.emu_gemm_entries
         g = workloads.rng(99)
         ii = g.integers(0, m, 256)
         jj = g.integers(0, n, 256)
         bb = np.zeros(256, dtype=np.int64)
-        step = lambda: oracle.emu_gemm_entries(args.mode, A, B, m, n, k, bb, ii, jj)  # noqa: E731
+        step = lambda: emu_entries(args.mode, A, B, m, n, k, bb, ii, jj)  # noqa: E731
         flops = 2.0 * k * 256
         sample = f"each step: 256 sampled outputs (full k) of the {m}x{n}x{k} GEMM"
     for _ in range(args.warmup):
@@ -225,12 +229,20 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
-def _config(cfg, mode, world):
-    return {"workload": f"{cfg.name}: {cfg.note}; {mode} split", "batch_per_gpu": cfg.batch,
-            "m": cfg.m, "n": cfg.n, "k": cfg.k, "split": mode, "inputs": "uniform[-1,1] FP32, seeded Philox",
-            "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
-            "l2": "no flush: inputs per step exceed the 126 MB L2" if
-                  4 * (cfg.m * cfg.k + cfg.k * cfg.n + cfg.m * cfg.n) * cfg.batch > 126e6 else "small"}
+def _config(cfg, mode, world, batch=None):
+    batch = cfg.batch if batch is None else batch
+    inputs = {"uniform": "uniform[-1,1] FP32", "logu30": "+-2^U(-30,30) FP32 (log-uniform magnitudes)"}[cfg.dist]
+    out = {"workload": f"{cfg.name}: {cfg.note}; {mode} split", "batch_per_gpu": batch,
+           "m": cfg.m, "n": cfg.n, "k": cfg.k, "split": mode, "inputs": inputs + ", seeded Philox",
+           "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
+           "l2": "no flush: inputs per step exceed the 126 MB L2" if
+                 4 * (cfg.m * cfg.k + cfg.k * cfg.n + cfg.m * cfg.n) * batch > 126e6 else
+                 "no flush: inputs (< L2) stay L2-resident across steps"}
+    if cfg.name == "c1":
+        out["timing"] = "one CUDA-graph replay (one launch) per step"
+    if cfg.name == "c4" and mode == "fp16":
+        out["entry"] = "emu_sgemm_batched_range (range-safe FP16, R#22)"
+    return out
 
 
 def run_c3_sharded(args, rank, world, local):
@@ -322,28 +334,51 @@ def main():
         run_c3_sharded(args, rank, world, local)
         return
     cfg = workloads.CONFIGS[args.config]
-    m, n, k, batch = cfg.m, cfg.n, cfg.k, cfg.batch
+    m, n, k = cfg.m, cfg.n, cfg.k
     mode = args.mode
+    # c5: a FIXED global batch split over the ranks (strong scaling);
+    # every other batched config: its batch per rank (weak scaling, R#21)
+    strong = args.config == "c5"
+    batch = cfg.batch // world if strong else cfg.batch
+    item0 = rank * batch
 
-    # inputs: this rank's contiguous block of problems (weak scaling)
-    item0, _ = shard(rank, world, batch)
-    A_h, B_h = workloads.make_operands(batch, m, n, k, cfg.seed, item0=item0)
+    # inputs: this rank's contiguous block of problems
+    A_h, B_h = workloads.make_operands(batch, m, n, k, cfg.seed, dist=cfg.dist, item0=item0)
     dA = torch.from_numpy(A_h).cuda()
     dB = torch.from_numpy(B_h).cuda()
     dC = torch.empty((batch, n, m), device="cuda")
     stream = torch.cuda.current_stream()
     sA, sB, sC = k * m, n * k, n * m
+    # c4 in FP16 mode: the range-safe entry (R#22; plain FP16 overflows at 2^30)
+    use_range = args.config == "c4" and mode == "fp16"
+    if use_range:
+        ws_bytes = emu.emu_range_workspace_size(m, n, batch)
+        ws = torch.empty(max(ws_bytes // 4, 4), dtype=torch.int32, device="cuda")
 
     launches = 0
 
     def step():
         nonlocal launches
-        emu.emu_sgemm_batched(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, stream)
+        if use_range:
+            emu.emu_sgemm_batched_range(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, ws,
+                                        ws_bytes, stream)
+        else:
+            emu.emu_sgemm_batched(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, stream)
         launches += emu.emu_last_launch_count()
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # c1 is launch-latency bound (16 x 64^3): each step is one replay of a CUDA graph
+    # holding the launch, so the host launch path is not what is timed
+    graph = None
+    if args.config == "c1":
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+        launches_per_step = emu.emu_last_launch_count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -352,7 +387,11 @@ def main():
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            if graph is not None:
+                graph.replay()
+                launches += launches_per_step
+            else:
+                step()
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -382,7 +421,7 @@ def main():
 
     # e2e through the C ABI with pinned HOST buffers (H2D + compute + D2H per step)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not use_range:   # (the host entry has no range-safe form)
         pA = torch.from_numpy(A_h).pin_memory()
         pB = torch.from_numpy(B_h).pin_memory()
         pC = torch.empty((batch, n, m)).pin_memory()
@@ -406,10 +445,13 @@ def main():
     # cuBLAS measurement): its roofline uses the sustained peak; the burst fraction is
     # reported beside it
     tc_peak_sus = peaks["bf16_tflops_sustained"] * (1.0 if mode == "fp16" else 0.5)
-    kname = ("emu_sgemm_pair_ts_kernel<%s, 128 cols, split commit%s>"
+    kname = ("emu_sgemm_pair_ts_kernel<%s, 128 cols, split commit%s%s>"
              % ("FP16" if mode == "fp16" else "TF32",
-                ", A-stationary" if (args.config == "c2" and (mode == "fp16" or k <= 128)) else ""))
-    if args.config == "c2":
+                ", A-stationary" if (args.config in ("c2", "c5") and (mode == "fp16" or k <= 128)) else "",
+                ", range-safe (+ range_max_kernel)" if use_range else ""))
+    if args.config == "c1":
+        kname = "emu_sgemm_kernel<%s, 128 cols> (m <= 128: single-CTA tiles)" % ("FP16" if mode == "fp16" else "TF32")
+    if args.config in ("c1", "c2", "c5"):
         bytes_launch = 4.0 * (m * k + k * n + m * n) * batch
         achieved = bytes_launch / (ms_per_step / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -435,8 +477,8 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": _config(cfg, mode, world),
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config(cfg, mode, world, batch),
         "frac_fp32_simt_peak": per_gpu / FP32_SIMT_PEAK_TF,
         "frac_tc_peak_over_3": per_gpu / (tc_peak / 3.0),
         "frac_tc_sustained_peak_over_3": per_gpu / (tc_peak_sus / 3.0),

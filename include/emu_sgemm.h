@@ -131,6 +131,25 @@ emu_status emu_sgemm_batched_t(char transa, char transb, int m, int n, int k, fl
                                unsigned int* d_range_flag, int kblock, unsigned int flags);
 
 /*
+ * emu_sgemm_batched_layout -- emu_sgemm_batched_t with a storage order (NEXT row 2,
+ * "row-major at the C ABI"; cblas_sgemm's Order argument):
+ *   EMU_COL_MAJOR: exactly emu_sgemm_batched_t.
+ *   EMU_ROW_MAJOR: every matrix is row-major: X(i, j) = X[i*ldX + j]; op(A) is m x k,
+ *     op(B) k x n, C m x n with ldc >= max(1, n); 'N' A needs lda >= max(1, k), 'T' A
+ *     (stored k x m) lda >= max(1, m); 'N' B ldb >= max(1, n), 'T' B (stored n x k)
+ *     ldb >= max(1, k).  Computed as the column-major C^T = op(B)^T op(A)^T (same
+ *     arithmetic per element; no data is moved).
+ * Another layout value -> EMU_STATUS_INVALID_VALUE; other errors as emu_sgemm_batched_t.
+ */
+typedef enum { EMU_COL_MAJOR = 0, EMU_ROW_MAJOR = 1 } emu_layout;
+emu_status emu_sgemm_batched_layout(emu_layout layout, char transa, char transb, int m, int n, int k,
+                                    float alpha, const float* A, int lda, long long strideA,
+                                    const float* B, int ldb, long long strideB,
+                                    float beta, float* C, int ldc, long long strideC,
+                                    int batch, emu_split_mode mode, void* stream,
+                                    unsigned int* d_range_flag, int kblock, unsigned int flags);
+
+/*
  * Range-safe mode (DESIGN R#22).  The paper splits raw
  * values, so FP16 mode overflows for |x| >= 65520 (R#4).  This
  * entry first scales row i of A_b by 2^-e_i and column j of B_b by 2^-f_j,

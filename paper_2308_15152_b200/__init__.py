@@ -17,7 +17,8 @@ __all__ = [
     "emu_sgemm", "emu_sgemm_batched", "emu_sgemm_batched_ex", "emu_sgemm_batched_host",
     "emu_split", "emu_status_string", "emu_version", "emu_last_launch_count", "mode_of",
     "EMU_FLAG_SIMT", "emu_tcec_gemm_batched", "emu_tcec_householder_batched", "emu_tcec_givens_batched",
-    "emu_tcec_scan", "emu_sgemm_multicast",
+    "emu_tcec_scan", "emu_sgemm_multicast", "EMU_COL_MAJOR", "EMU_ROW_MAJOR", "emu_sgemm_batched_layout",
+    "matmul",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libemusgemm.so")
@@ -26,6 +27,8 @@ EMU_SPLIT_FP16 = 0
 EMU_SPLIT_TF32 = 1
 EMU_FLAG_NO_CORRECTION = 1
 EMU_FLAG_SIMT = 2
+EMU_COL_MAJOR = 0
+EMU_ROW_MAJOR = 1
 STATUS = {0: "SUCCESS", 1: "INVALID_VALUE", 2: "NOT_SUPPORTED", 3: "ARCH_MISMATCH",
           4: "LAUNCH_FAILED", 5: "CUDA_ERROR"}
 
@@ -72,6 +75,8 @@ lib.emu_tcec_givens_batched.argtypes = [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i,
 lib.emu_tcec_givens_batched.restype = _i
 lib.emu_tcec_scan.argtypes = [_i, _i, _p, _i, _p, _i, _i, _p, _u]
 lib.emu_tcec_scan.restype = _i
+lib.emu_sgemm_batched_layout.argtypes = [_i, ctypes.c_char, ctypes.c_char] + _GEMM_ARGS + [_p, _i, _u]
+lib.emu_sgemm_batched_layout.restype = _i
 lib.emu_sgemm_multicast.argtypes = [_i, _i, _i, _f, _p, _i, _p, _i, ctypes.POINTER(_p), _i, _i, _i, _p, _i, _u]
 lib.emu_sgemm_multicast.restype = _i
 lib.emu_status_string.argtypes = [_i]
@@ -195,6 +200,58 @@ def emu_tcec_givens_batched(m, n, i, j, CS, X, ldx, strideX, C, ldc, strideC, ba
 def emu_tcec_scan(n, count, X, ldx, Y, ldy, mode, stream=None, flags=0):
     _check(lib.emu_tcec_scan(n, count, _ptr(X), ldx, _ptr(Y), ldy, mode_of(mode), _stream(stream), flags),
            "emu_tcec_scan")
+
+
+def emu_sgemm_batched_layout(layout, transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C,
+                             ldc, strideC, batch, mode, stream=None, range_flag=None, kblock=0, flags=0):
+    _check(lib.emu_sgemm_batched_layout(layout, transa.encode() if isinstance(transa, str) else transa,
+                                        transb.encode() if isinstance(transb, str) else transb,
+                                        m, n, k, alpha, _ptr(A), lda, strideA, _ptr(B), ldb, strideB,
+                                        beta, _ptr(C), ldc, strideC, batch, mode_of(mode), _stream(stream),
+                                        _ptr(range_flag), kblock, flags),
+           "emu_sgemm_batched_layout")
+
+
+def _rm_operand(x, name):
+    """(trans, ld, batch stride) of a row-major 2-D / 3-D float32 CUDA tensor view:
+    'N' when rows are contiguous, 'T' when columns are (a transposed view)."""
+    import torch
+    if x.dtype != torch.float32 or not x.is_cuda or x.dim() not in (2, 3):
+        raise TypeError(f"{name}: a 2-D or 3-D float32 CUDA tensor is required")
+    r, c = x.stride()[-2], x.stride()[-1]
+    rows, cols = x.shape[-2], x.shape[-1]
+    sb = x.stride()[0] if x.dim() == 3 else 0
+    if c == 1 and r >= max(1, cols):
+        return "N", r, sb
+    if r == 1 and c >= max(1, rows):
+        return "T", c, sb
+    raise ValueError(f"{name}: rows or columns must be contiguous")
+
+
+def matmul(A, B, mode="fp16", out=None, stream=None):
+    """C = A @ B for float32 CUDA tensors (torch.matmul semantics for 2-D / 3-D
+    operands; a 2-D operand is shared by every problem of a 3-D one), emulated by
+    the library: one emu_sgemm_batched_layout call (row-major), nothing computed here."""
+    import torch
+    ta, lda, sA = _rm_operand(A, "A")
+    tb, ldb, sB = _rm_operand(B, "B")
+    m, k = A.shape[-2], A.shape[-1]
+    k2, n = B.shape[-2], B.shape[-1]
+    if k != k2:
+        raise ValueError(f"inner dimensions differ: {k} vs {k2}")
+    batch = A.shape[0] if A.dim() == 3 else (B.shape[0] if B.dim() == 3 else 1)
+    if A.dim() == 3 and B.dim() == 3 and A.shape[0] != B.shape[0]:
+        raise ValueError("batch sizes differ")
+    shape = (batch, m, n) if (A.dim() == 3 or B.dim() == 3) else (m, n)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=A.device)
+    elif tuple(out.shape) != shape or not out.is_contiguous():
+        raise ValueError("out must be a contiguous tensor of the result shape")
+    if out.numel() == 0:
+        return out
+    emu_sgemm_batched_layout(EMU_ROW_MAJOR, ta, tb, m, n, k, 1.0, A, lda, sA, B, ldb, sB, 0.0, out, max(1, n),
+                             m * n, batch, mode, stream)
+    return out
 
 
 def emu_sgemm_multicast(m, n, k, alpha, A, lda, B, ldb, C_dst, ldc, mode, stream=None, kblock=0, flags=0):

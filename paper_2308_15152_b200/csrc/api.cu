@@ -676,6 +676,23 @@ __attribute__((visibility("default"))) emu_status emu_sgemm_batched_t(char trans
                      d_range_flag, kblock, flags, nullptr, 0, ta, tb);
 }
 
+// row-major storage (NEXT row 2): a row-major X with leading dimension ld is the
+// column-major X^T with the same ld, so C = op(A) op(B) row-major is
+// C^T = op(B)^T op(A)^T column-major -- the operands swap, the trans flags stay
+__attribute__((visibility("default"))) emu_status emu_sgemm_batched_layout(
+    emu_layout layout, char transa, char transb, int m, int n, int k, float alpha, const float* A, int lda,
+    long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc, long long strideC,
+    int batch, emu_split_mode mode, void* stream, unsigned int* d_range_flag, int kblock, unsigned int flags)
+{
+    g_last_launches = 0;
+    if (layout == EMU_COL_MAJOR)
+        return emu_sgemm_batched_t(transa, transb, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc,
+                                   strideC, batch, mode, stream, d_range_flag, kblock, flags);
+    if (layout != EMU_ROW_MAJOR) return EMU_STATUS_INVALID_VALUE;
+    return emu_sgemm_batched_t(transb, transa, n, m, k, alpha, B, ldb, strideB, A, lda, strideA, beta, C, ldc,
+                               strideC, batch, mode, stream, d_range_flag, kblock, flags);
+}
+
 __attribute__((visibility("default"))) size_t emu_range_workspace_size(int m, int n, int batch)
 {
     if (m < 0 || n < 0 || batch < 0) return 0;

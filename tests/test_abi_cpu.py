@@ -178,3 +178,19 @@ def test_multicast_validation(emu):
     bad = (ct.c_void_p * 2)(16, None)
     assert L.emu_sgemm_multicast(8, 8, 8, 1.0, 16, 8, 16, 8, bad, 2, 8, 0, None, 0, 0) == 1
     assert L.emu_sgemm_multicast(-1, 8, 8, 1.0, 16, 8, 16, 8, arr, 2, 8, 0, None, 0, 0) == 1
+
+
+def test_layout_entry_validation(emu):
+    L = emu.lib
+    args = [b"N", b"N", 8, 16, 32, 1.0, 16, 32, 0, 16, 16, 0, 0.0, 16, 16, 0, 1, 0, None, None, 0, 0]
+    assert L.emu_sgemm_batched_layout(2, *args) == 1                 # unknown layout
+    bad = list(args)
+    bad[7] = 31                                                      # row-major 'N' A: lda >= k = 32
+    assert L.emu_sgemm_batched_layout(1, *bad) == 1
+    bad = list(args)
+    bad[14] = 15                                                     # row-major C: ldc >= n = 16
+    assert L.emu_sgemm_batched_layout(1, *bad) == 1
+    assert L.emu_sgemm_batched_layout(1, b"X", b"N", *args[2:]) == 1
+    empty = list(args)
+    empty[16] = 0                                                    # batch 0
+    assert L.emu_sgemm_batched_layout(1, *empty) == 0
