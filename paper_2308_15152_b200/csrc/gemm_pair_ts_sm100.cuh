@@ -228,68 +228,80 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 PROF_ADD(P_MMA_WAIT_ACC);
                                 TRACE_AT(1, 5, kb);
                                 ptx::tc_fence_after();
-                                uint32_t s = s0, ph = ph0;
-                                for (int ks = ks0; ks < ks1; ++ks) {
+                                // a k-block longer than the operand ring (kb_stages > SOP) is
+                                // issued in chunks of <= SOP stages: P2 + P3 of a chunk, then its
+                                // P1 (which frees the chunk's slots); D_corr is committed before
+                                // the last chunk's P1, so its drain still overlaps P1.  Each
+                                // accumulator sees its stages in ascending order either way.
+                                for (int c0 = ks0; c0 < ks1; c0 += Cfg::SOP) {
+                                    const int c1 = min(c0 + Cfg::SOP, ks1);
+                                    uint32_t s = s0, ph = ph0;
+                                    for (int ks = c0; ks < c1; ++ks) {
+                                        PROF_T0();
+                                        ptx::mbar_wait(&op_full[s], ph);
+                                        PROF_ADD(P_MMA_WAIT_OP);
+                                        TRACE_AT(1, 9, ks);
+                                        ptx::tc_fence_after();
+                                        PROF_T0();
+                                        if (p.corr) {
+                                            const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
+                                            const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                                            const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                                            for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                                const uint64_t dB_hi =
+                                                    ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                                const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32,
+                                                                                      16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                                const uint32_t ka = st * Cfg::KCOLS;
+                                                const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                                if (MODE == 0) {
+                                                    ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);   // P2
+                                                    ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);    // P3
+                                                } else {
+                                                    ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
+                                                    ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
+                                                }
+                                            }
+                                        }
+                                        PROF_ADD(P_MMA_ISSUE);
+                                        if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                                    }
+                                    if (c1 == ks1) {
+                                        ptx::tc_commit_pair(&acc_full[1], 0x3);
+                                        TRACE_AT(1, 6, kb);
+                                    }
+                                    if (c0 == ks0) {
+                                        PROF_T0();
+                                        ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
+                                        PROF_ADD(P_MMA_WAIT_ACC);
+                                        TRACE_AT(1, 7, kb);
+                                        ptx::tc_fence_after();
+                                    }
                                     PROF_T0();
-                                    ptx::mbar_wait(&op_full[s], ph);
-                                    PROF_ADD(P_MMA_WAIT_OP);
-                                    TRACE_AT(1, 9, ks);
-                                    ptx::tc_fence_after();
-                                    PROF_T0();
-                                    if (p.corr) {
+                                    s = s0; ph = ph0;
+                                    for (int ks = c0; ks < c1; ++ks) {
                                         const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
-                                        const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
                                         const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
 #pragma unroll
                                         for (int st = 0; st < Cfg::NSTEPS; ++st) {
                                             const uint64_t dB_hi =
                                                 ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                            const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
-                                                                                  Cfg::B_SBO, Cfg::B_LAYOUT);
-                                            const uint32_t ka = st * Cfg::KCOLS;
                                             const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
-                                            if (MODE == 0) {
-                                                ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);   // P2
-                                                ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);    // P3
-                                            } else {
-                                                ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
-                                                ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
-                                            }
+                                            if (MODE == 0)
+                                                ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
+                                            else
+                                                ptx::mma_tf32_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);
                                         }
+                                        ptx::tc_commit_pair(&op_empty[s], 0x3);   // B (and non-stationary A) slot free
+                                        if (lastA) ptx::tc_commit_pair(&aslot_empty[ks], 0x3);
+                                        if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                                     }
-                                    PROF_ADD(P_MMA_ISSUE);
-                                    if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
-                                }
-                                ptx::tc_commit_pair(&acc_full[1], 0x3);
-                                TRACE_AT(1, 6, kb);
-                                PROF_T0();
-                                ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
-                                PROF_ADD(P_MMA_WAIT_ACC);
-                                TRACE_AT(1, 7, kb);
-                                ptx::tc_fence_after();
-                                PROF_T0();
-                                s = s0; ph = ph0;
-                                for (int ks = ks0; ks < ks1; ++ks) {
-                                    const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
-                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
-#pragma unroll
-                                    for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                        const uint64_t dB_hi =
-                                            ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                        const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
-                                        if (MODE == 0)
-                                            ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
-                                        else
-                                            ptx::mma_tf32_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);
-                                    }
-                                    ptx::tc_commit_pair(&op_empty[s], 0x3);   // B (and non-stationary A) slot free
-                                    if (lastA) ptx::tc_commit_pair(&aslot_empty[ks], 0x3);
-                                    if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                                    s0 = s; ph0 = ph;
                                 }
                                 ptx::tc_commit_pair(&acc_full[0], 0x3);
                                 PROF_ADD(P_MMA_ISSUE);
                                 TRACE_AT(1, 8, kb);
-                                s0 = s; ph0 = ph;
                             }
                         }
                     }

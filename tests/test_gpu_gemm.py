@@ -91,8 +91,11 @@ def test_parity_uniform(mode, shape):
 
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("kblock", [32, 64, 256, 4096])
-def test_parity_kblock(mode, kblock):
-    m, n, k = 128, 128, 1024
+@pytest.mark.parametrize("m", [128, 384])   # single-CTA kernel / CTA-pair TS kernel
+def test_parity_kblock(mode, kblock, m):
+    """every combine interval the header allows, on both kernel families; in the TS
+    kernel a k-block longer than the operand ring (KB > 128) is issued in chunks"""
+    n, k = 256, 1024
     A, B = workloads.make_operands(1, m, n, k, seed=77)
     _cmp(mode, A, B, m, n, k, kblock=kblock)
 
