@@ -32,6 +32,10 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 MODE_FP16 = 0
 MODE_TF32 = 1
+# "sm100" tensor-core model parameters (R#9): products per aligned
+# group, extra alignment bits below the largest term's 24-bit significand
+TC_GROUP = 16   # >= K_inst: one fused sum per MMA instruction
+TC_EXTRA = 2
 _MODES = {"fp16": MODE_FP16, "tf32": MODE_TF32, MODE_FP16: MODE_FP16, MODE_TF32: MODE_TF32}
 
 BUILD_CMD = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
@@ -83,6 +87,7 @@ def lib():
         L.orc_sgemm_f32_batched.argtypes = [i32, i32, i32, f32, P, i64, i64, P, i64, i64,
                                             f32, P, i64, i64, i32]
         L.orc_sgemm_f32_batched.restype = None
+        L.orc_set_tc_model.argtypes = [i32, i32]; L.orc_set_tc_model.restype = None
         L.orc_max_threads.argtypes = []; L.orc_max_threads.restype = i32
         L.orc_set_threads.argtypes = [i32]; L.orc_set_threads.restype = None
         _lib = L
@@ -172,6 +177,22 @@ def reconstruct(mode, hi_val, lo_val):
 
 
 # ----------------------------------------------------------------- gemm ----
+# Tensor-core accumulation models for the block sums of O3 (oracle.c, R#9):
+#   "ideal": exact block sum, one RN to binary32;
+#   "sm100": per MMA instruction, its products and the accumulator aligned to
+#            the largest (un-normalised) exponent with F extra bits, truncated,
+#            summed, RZ to binary32 (the paper's RZ; the alignment width
+#            identified on B200 by tools/tc_fit.py, R#9).
+#   "simt":  one binary32 FMA per product, k ascending (the device API's
+#            CUDA-core policy, R#26).
+TC_MODELS = {"ideal": (0, 0), "sm100": (TC_GROUP, TC_EXTRA), "simt": (-1, 0)}
+
+
+def _set_tc(tc):
+    g, f = TC_MODELS[tc]
+    lib().orc_set_tc_model(g, f)
+
+
 def _batched_args(A, B, m, n, k):
     A = _f32(A)
     B = _f32(B)
@@ -188,10 +209,11 @@ def _batched_args(A, B, m, n, k):
     return A, B, batch, lda, ldb, sA, sB
 
 
-def emu_gemm(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True, ldc=None):
+def emu_gemm(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True, ldc=None, tc="ideal"):
     """Emulation model O3 over column-major batched operands; returns C as
     (batch, n, ldc) float32.  beta == 0 never reads C."""
     mode = _MODES[mode]
+    _set_tc(tc)
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:
@@ -206,8 +228,9 @@ def emu_gemm(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True,
 
 
 def emu_gemm_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=None,
-                     kb=64, corr=True, ldc=None):
+                     kb=64, corr=True, ldc=None, tc="ideal"):
     mode = _MODES[mode]
+    _set_tc(tc)
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:
@@ -228,10 +251,11 @@ def emu_gemm_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=N
     return out
 
 
-def emu_gemm_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True, ldc=None):
+def emu_gemm_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True, ldc=None, tc="ideal"):
     """Range-safe mode (DESIGN R#22): per-row / per-column
     power-of-two pre-scaling around the unchanged emulation model."""
     mode = _MODES[mode]
+    _set_tc(tc)
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:
@@ -246,8 +270,9 @@ def emu_gemm_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr
 
 
 def emu_gemm_range_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=None,
-                           kb=64, corr=True, ldc=None):
+                           kb=64, corr=True, ldc=None, tc="ideal"):
     mode = _MODES[mode]
+    _set_tc(tc)
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:

@@ -37,6 +37,19 @@ def emu_gpu(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kblock=0, flags=0,
     return dC.cpu().numpy()
 
 
+def assert_bits_equal(got, want):
+    """element-wise equality by value (-0 == +0; NaN == NaN), with a readable
+    report of the first mismatches"""
+    got = np.asarray(got, dtype=np.float32)
+    want = np.asarray(want, dtype=np.float32)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    bad = ~((got == want) | (np.isnan(got) & np.isnan(want)))
+    if np.any(bad):
+        idx = np.argwhere(bad)[:5]
+        rows = [(tuple(int(v) for v in ix), float(got[tuple(ix)]), float(want[tuple(ix)])) for ix in idx]
+        raise AssertionError(f"{int(bad.sum())} of {bad.size} outputs differ from the oracle: {rows}")
+
+
 def tolerance(mode, A, B, m, n, k, kblock=64):
     """Element-wise bound on |C_gpu - C_oracle|: the tensor
     core's own accumulation of each k-block (at most 2 binary32 ulps per MMA

@@ -5,8 +5,10 @@ Bars:
   * bit-exact where the method's result is exact: identity / permutation
     operands (C == reconstruct(split(B))), small-integer operands (exact
     integer product), quick returns;
-  * elsewhere |C_gpu - C_oracle| <= gamma u (|A||B|)_ij (tests/gpu_util.py),
-    the tensor core's in-block accumulation being the only freedom;
+  * elsewhere |C_gpu - C_oracle| <= gamma u (|A||B|)_ij (tests/gpu_util.py)
+    against the "ideal" block sums, the tensor core's in-block accumulation
+    being the only freedom; and bit for bit against the oracle's measured
+    tensor-core model (tc="sm100", R#9);
   * north_star's accuracy gate vs FP64: rel-Frobenius <= 2x plain FP32 SGEMM
     and <= 1e-5 for k <= 4096, uniform[-1,1].
 """
@@ -17,7 +19,7 @@ import pytest
 
 import oracle
 import workloads
-from gpu_util import emu_gpu, tolerance
+from gpu_util import assert_bits_equal, emu_gpu, tolerance
 
 pytestmark = pytest.mark.gpu
 MODES = ["fp16", "tf32"]
@@ -35,6 +37,11 @@ def _cmp(mode, A, B, m, n, k, kblock=0, **kw):
     d = np.abs(C[..., :m].astype(np.float64) - ref[..., :m].astype(np.float64))
     ratio = np.max(d / np.where(tol > 0, tol, 1.0))
     assert np.all(d <= tol), f"max |gpu-oracle|/tol = {ratio:.3g}"
+    # bit-exact with the oracle's measured tensor-core model (R#9)
+    hw = oracle.emu_gemm(mode, A, B, m, n, k, kb=kb, alpha=kw.get("alpha", 1.0),
+                         beta=kw.get("beta", 0.0), C=kw.get("C"),
+                         corr=not (kw.get("flags", 0) & 1), tc="sm100")
+    assert_bits_equal(C[..., :m], hw[..., :m])
     return C, ref
 
 
@@ -285,6 +292,7 @@ def _sampled(mode, batch, m, n, k, seed, nsamp=384):
     gamma = 2 * (64 / (16 if mode == "fp16" else 8)) + 4 + 2 * math.ceil(k / 64)
     tol = gamma * 2.0 ** -24 * absab
     assert np.all(np.abs(got.astype(np.float64) - ref) <= tol)
+    assert_bits_equal(got, oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="sm100"))
     return A, B
 
 

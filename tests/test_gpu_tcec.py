@@ -13,7 +13,7 @@ import pytest
 import oracle
 import workloads
 from oracle import structured
-from gpu_util import tolerance
+from gpu_util import assert_bits_equal, tolerance
 
 pytestmark = pytest.mark.gpu
 MODES = ["fp16", "tf32"]
@@ -61,6 +61,9 @@ def test_tcec_gemm_parity(mode, flags):
     tol = (_simt_tol if flags & SIMT else tolerance)(mode, A, B, m, n, k)
     err = np.abs(C.astype(np.float64) - ref)
     assert np.all(err <= tol), np.max(err / tol)
+    # bit for bit with the oracle's model of the backend (R#9 / R#26)
+    assert_bits_equal(C, oracle.emu_gemm(mode, A, B, m, n, k, corr=not (flags & NO_CORR),
+                                         tc="simt" if flags & SIMT else "sm100"))
     if not flags & NO_CORR:
         R = oracle.gemm_f64(A, B, m, n, k)
         assert oracle.rel_frobenius(C, R) <= 2 * oracle.rel_frobenius(oracle.sgemm_f32(A, B, m, n, k), R)
@@ -92,6 +95,8 @@ def test_tcec_gemm_alpha_beta_and_kblock(mode):
         ref = oracle.emu_gemm(mode, A, B, m, n, k, alpha=0.5, beta=-1.5, C=C0, kb=kb or 64)
         tol = 0.5 * tolerance(mode, A, B, m, n, k, kblock=kb or 64) + 2 * U * np.abs(ref)
         assert np.all(np.abs(C.astype(np.float64) - ref) <= tol)
+        assert_bits_equal(C, oracle.emu_gemm(mode, A, B, m, n, k, alpha=0.5, beta=-1.5, C=C0, kb=kb or 64,
+                                             tc="sm100"))
 
 
 @pytest.mark.parametrize("mode", MODES)
