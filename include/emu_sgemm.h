@@ -99,8 +99,9 @@ emu_status emu_sgemm(int m, int n, int k, float alpha,
  *   d_range_flag: NULL, or a device unsigned int that the kernel ORs with 1
  *     (sticky, never cleared) when an FP16-mode operand element has
  *     |x| >= 65520 or is not finite (its hi part is +-Inf/NaN, R#4);
- *   kblock: the combine interval KB in k (0 = default 64; otherwise a positive
- *     multiple of 32, at most 4096);
+ *   kblock: the combine interval KB in k (R#7; 0 = the default: 64 for
+ *     k <= 8192, doubled for every further factor 4 of k -- 128 for k <= 32768,
+ *     256 for k <= 131072, ...; otherwise a positive multiple of 32, at most 4096);
  *   flags: EMU_FLAG_* bits (0 = the paper's method).
  */
 emu_status emu_sgemm_batched_ex(int m, int n, int k, float alpha,

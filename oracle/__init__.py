@@ -188,6 +188,15 @@ def reconstruct(mode, hi_val, lo_val):
 TC_MODELS = {"ideal": (0, 0), "sm100": (TC_GROUP, TC_EXTRA), "simt": (-1, 0)}
 
 
+def default_kb(k: int) -> int:
+    """the library's default combine interval (R#7): 64 for k <= 8192,
+    doubled for every further factor 4 of k, at most 4096"""
+    kb, lim = 64, 8192
+    while k > lim and kb < 4096:
+        kb, lim = kb * 2, lim * 4
+    return kb
+
+
 def _set_tc(tc):
     g, f = TC_MODELS[tc]
     lib().orc_set_tc_model(g, f)
@@ -209,11 +218,12 @@ def _batched_args(A, B, m, n, k):
     return A, B, batch, lda, ldb, sA, sB
 
 
-def emu_gemm(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True, ldc=None, tc="ideal"):
+def emu_gemm(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=None, corr=True, ldc=None, tc="ideal"):
     """Emulation model O3 over column-major batched operands; returns C as
     (batch, n, ldc) float32.  beta == 0 never reads C."""
     mode = _MODES[mode]
     _set_tc(tc)
+    kb = default_kb(k) if not kb else kb
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:
@@ -228,9 +238,10 @@ def emu_gemm(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True,
 
 
 def emu_gemm_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=None,
-                     kb=64, corr=True, ldc=None, tc="ideal"):
+                     kb=None, corr=True, ldc=None, tc="ideal"):
     mode = _MODES[mode]
     _set_tc(tc)
+    kb = default_kb(k) if not kb else kb
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:
@@ -251,11 +262,12 @@ def emu_gemm_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=N
     return out
 
 
-def emu_gemm_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr=True, ldc=None, tc="ideal"):
+def emu_gemm_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=None, corr=True, ldc=None, tc="ideal"):
     """Range-safe mode (DESIGN R#22): per-row / per-column
     power-of-two pre-scaling around the unchanged emulation model."""
     mode = _MODES[mode]
     _set_tc(tc)
+    kb = default_kb(k) if not kb else kb
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:
@@ -270,9 +282,10 @@ def emu_gemm_range(mode, A, B, m, n, k, alpha=1.0, beta=0.0, C=None, kb=64, corr
 
 
 def emu_gemm_range_entries(mode, A, B, m, n, k, bidx, ii, jj, alpha=1.0, beta=0.0, C=None,
-                           kb=64, corr=True, ldc=None, tc="ideal"):
+                           kb=None, corr=True, ldc=None, tc="ideal"):
     mode = _MODES[mode]
     _set_tc(tc)
+    kb = default_kb(k) if not kb else kb
     A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
     ldc = m if ldc is None else ldc
     if C is None:

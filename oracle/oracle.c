@@ -27,6 +27,14 @@
  *                       exponents are 0; exact scale equivariance (row i of A
  *                       times 2^t => row i of C times 2^t, bit for bit); small
  *                       integers exact; the accuracy gate on 2^-30..2^30 inputs
+ *   tc_instr ("sm100")  the paper's RZ vector, exact results on
+ *                       identity/permutation/small-integer operands, the
+ *                       truncation-only bound below the exact sum (positive
+ *                       terms) and the signed-term bound vs Fractions, odd
+ *                       symmetry (tests/test_oracle_tc_model.py); its alignment
+ *                       width is the hardware's, measured (R#9)
+ *   "simt" model        equals the sequential-FMA SGEMM (O5) on split-exact
+ *                       operands with k <= KB
  * Parity unpinned: none of the functions above.
  *
  * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -fPIC

@@ -461,6 +461,23 @@ __attribute__((visibility("default"))) int emu_version(void) { return EMU_VERSIO
 
 __attribute__((visibility("default"))) int emu_last_launch_count(void) { return g_last_launches; }
 
+// default combine interval KB (R#7): 64 up to k = 8192, doubled for every further
+// factor 4 of k (128 up to 32768, ...).  With the measured tensor-core model the
+// error at k = 16384 is 0.12x (FP16) / 0.17x (TF32) plain SGEMM at KB = 128 against
+// 0.14x / 0.15x at 64 (tools/kb_accuracy.py): the cross-block FP32 additions
+// dominate there, so the longer interval costs nothing in accuracy and halves the
+// combine work
+static int default_kblock(int k)
+{
+    int kb = 64;
+    long long lim = 8192;
+    while (k > lim && kb < 4096) {
+        kb *= 2;
+        lim *= 4;
+    }
+    return kb;
+}
+
 // the device entries; range_ws != nullptr selects the range-safe mode (R#22)
 static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
                             const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
@@ -478,6 +495,7 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     if (strideA < 0 || strideB < 0 || strideC < 0) return EMU_STATUS_INVALID_VALUE;
     if (kblock < 0 || (kblock > 0 && (kblock % 32 != 0 || kblock > 4096))) return EMU_STATUS_INVALID_VALUE;
     if (flags & ~EMU_FLAG_NO_CORRECTION) return EMU_STATUS_INVALID_VALUE;
+    if (kblock == 0) kblock = default_kblock(k);
     if (m == 0 || n == 0 || batch == 0) return EMU_STATUS_SUCCESS;
     if (C == nullptr) return EMU_STATUS_INVALID_VALUE;
     if (batch > 1 && strideC < (long long)ldc * n) return EMU_STATUS_INVALID_VALUE;

@@ -50,14 +50,14 @@ def assert_bits_equal(got, want):
         raise AssertionError(f"{int(bad.sum())} of {bad.size} outputs differ from the oracle: {rows}")
 
 
-def tolerance(mode, A, B, m, n, k, kblock=64):
+def tolerance(mode, A, B, m, n, k, kblock=0):
     """Element-wise bound on |C_gpu - C_oracle|: the tensor
     core's own accumulation of each k-block (at most 2 binary32 ulps per MMA
     instruction of K_inst products plus the block's final alignment), and one
     ulp per cross-block add of the two differently-rounded running sums:
         gamma = 2*(KB/K_inst) + 4 + 2*ceil(k/KB),  tol = gamma * u * (|A||B|)_ij
     """
-    kb = kblock or 64
+    kb = kblock or oracle.default_kb(k)
     kinst = 16 if mode in (0, "fp16") else 8
     gamma = 2 * (kb / kinst) + 4 + 2 * math.ceil(max(k, 1) / kb)
     A = np.asarray(A)

@@ -29,7 +29,7 @@ def _logu(shape, lo, hi, seed):
 
 def _check(mode, A, B, m, n, k, kblock=0, **kw):
     C = emu_gpu(mode, A, B, m, n, k, kblock=kblock, **kw)
-    want = oracle.emu_gemm(mode, A, B, m, n, k, kb=kblock or 64, alpha=kw.get("alpha", 1.0),
+    want = oracle.emu_gemm(mode, A, B, m, n, k, kb=kblock or oracle.default_kb(k), alpha=kw.get("alpha", 1.0),
                            beta=kw.get("beta", 0.0), C=kw.get("C"), corr=not (kw.get("flags", 0) & 1),
                            tc="sm100")
     assert_bits_equal(C[..., :m], want[..., :m])
@@ -110,3 +110,14 @@ def test_range_safe_mode(mode):
     B = _logu((1, n, k), -30, 30, seed=951)
     C = emu_gpu_range(mode, A, B, m, n, k)
     assert_bits_equal(C, oracle.emu_gemm_range(mode, A, B, m, n, k, tc="sm100"))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_default_kblock_rule(mode):
+    """kblock = 0 selects KB = 128 above k = 8192 (R#7): identical bits to an
+    explicit 128, and to the oracle's own default"""
+    m, n, k = 256, 128, 8224
+    A, B = workloads.make_operands(1, m, n, k, seed=960)
+    C = emu_gpu(mode, A, B, m, n, k)
+    assert np.array_equal(C, emu_gpu(mode, A, B, m, n, k, kblock=128))
+    assert_bits_equal(C, oracle.emu_gemm(mode, A, B, m, n, k, tc="sm100"))

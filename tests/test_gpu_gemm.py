@@ -27,7 +27,7 @@ MODES = ["fp16", "tf32"]
 
 def _cmp(mode, A, B, m, n, k, kblock=0, **kw):
     C = emu_gpu(mode, A, B, m, n, k, kblock=kblock, **kw)
-    kb = kblock or 64
+    kb = kblock or oracle.default_kb(k)
     ref = oracle.emu_gemm(mode, A, B, m, n, k, kb=kb, alpha=kw.get("alpha", 1.0),
                           beta=kw.get("beta", 0.0), C=kw.get("C"),
                           corr=not (kw.get("flags", 0) & 1))
@@ -55,11 +55,11 @@ def test_identity_and_permutation_bit_exact(mode, kblock):
     for P in (np.eye(k, dtype=np.float32), np.eye(k, dtype=np.float32)[perm]):
         A = workloads.colmajor(P)[None]
         C = emu_gpu(mode, A, B, m, n, k, kblock=kblock)
-        ref = oracle.emu_gemm(mode, A, B, m, n, k, kb=kblock or 64)
+        ref = oracle.emu_gemm(mode, A, B, m, n, k, kb=kblock or oracle.default_kb(k))
         assert np.array_equal(C, ref)
         # B = P: C == reconstruct(split(A))
         C2 = emu_gpu(mode, B, workloads.colmajor(P)[None], m, n, k, kblock=kblock)
-        ref2 = oracle.emu_gemm(mode, B, workloads.colmajor(P)[None], m, n, k, kb=kblock or 64)
+        ref2 = oracle.emu_gemm(mode, B, workloads.colmajor(P)[None], m, n, k, kb=kblock or oracle.default_kb(k))
         assert np.array_equal(C2, ref2)
 
 
@@ -289,7 +289,8 @@ def _sampled(mode, batch, m, n, k, seed, nsamp=384):
     ref = oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j)
     absab = np.array([np.dot(np.abs(A[bb, :, ii].astype(np.float64)), np.abs(B[bb, jj, :].astype(np.float64)))
                       for bb, ii, jj in zip(b, i, j)])
-    gamma = 2 * (64 / (16 if mode == "fp16" else 8)) + 4 + 2 * math.ceil(k / 64)
+    kb = oracle.default_kb(k)
+    gamma = 2 * (kb / (16 if mode == "fp16" else 8)) + 4 + 2 * math.ceil(k / kb)
     tol = gamma * 2.0 ** -24 * absab
     assert np.all(np.abs(got.astype(np.float64) - ref) <= tol)
     assert_bits_equal(got, oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="sm100"))

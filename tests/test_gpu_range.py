@@ -16,7 +16,7 @@ MODES = ["fp16", "tf32"]
 
 def _cmp(mode, A, B, m, n, k, kblock=0, **kw):
     C = emu_gpu_range(mode, A, B, m, n, k, kblock=kblock, **kw)
-    kb = kblock or 64
+    kb = kblock or oracle.default_kb(k)
     ref = oracle.emu_gemm_range(mode, A, B, m, n, k, kb=kb, alpha=kw.get("alpha", 1.0),
                                 beta=kw.get("beta", 0.0), C=kw.get("C"), corr=not (kw.get("flags", 0) & 1))
     tol = tolerance(mode, A, B, m, n, k, kb) * abs(kw.get("alpha", 1.0))

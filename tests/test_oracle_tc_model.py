@@ -144,3 +144,11 @@ def test_simt_model_is_sequential_fma_sgemm(mode):
     B = v[1, :k * n].reshape(n, k)
     got = oracle.emu_gemm(mode, A, B, m, n, k, tc="simt")
     np.testing.assert_array_equal(got, oracle.sgemm_f32(A, B, m, n, k))
+
+
+def test_default_kb_table():
+    """R#7's default combine interval, as documented in include/emu_sgemm.h"""
+    table = {1: 64, 4096: 64, 8192: 64, 8193: 128, 16384: 128, 32768: 128, 32769: 256,
+             131072: 256, 131073: 512}
+    for k, kb in table.items():
+        assert oracle.default_kb(k) == kb, k
