@@ -371,6 +371,12 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
             if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
                 return EMU_STATUS_CUDA_ERROR;
+            if constexpr (!RANGE && !TA && !TB) {
+                if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Cfg::SMEM_BYTES) != cudaSuccess)
+                    return EMU_STATUS_CUDA_ERROR;
+            }
             g_dev[dev].ts_attr_set[slot] = true;
         }
     }
@@ -434,8 +440,21 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     p.unit_tiles = ASTAT ? p.tiles_n : 1;
     if (ASTAT && p.num_k_stages > Cfg::ASLOTS) return EMU_STATUS_NOT_SUPPORTED;   // dispatch guarantees it
     const long long clusters = std::min<long long>(p.num_units, sms / 2);
-    emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>
-        <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+    // the multicast epilogue is its own instantiation (MC): the plain kernels carry no
+    // per-destination loop
+    bool launched = false;
+    if constexpr (!RANGE && !TA && !TB) {
+        if (p.num_dst > 1) {
+            emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true>
+                <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+            launched = true;
+        }
+    }
+    if (!launched) {
+        if (p.num_dst > 1) return EMU_STATUS_NOT_SUPPORTED;
+        emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>
+            <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+    }
     g_last_launches = 1;
     return launch_status(cudaGetLastError());
 }
@@ -624,12 +643,15 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
 #undef EMU_RUN_T3
 #undef EMU_RUN_TT
     if (ts) {
+        // RANGE instantiations carry the overflow flag and the range-safe scaling; the
+        // plain ones (the paper's method) carry neither
         emu_status rs;
         if (mode == EMU_SPLIT_FP16) {
-            if (d_range_flag) EMU_RUN_TS(0, true);
+            if (d_range_flag || range) EMU_RUN_TS(0, true);
             else EMU_RUN_TS(0, false);
         } else {
-            EMU_RUN_TS(1, false);
+            if (range) EMU_RUN_TS(1, true);
+            else EMU_RUN_TS(1, false);
         }
         if (range && rs == EMU_STATUS_SUCCESS) g_last_launches = 2;   // max-|x| pass + GEMM
         return rs;

@@ -109,7 +109,10 @@ __device__ __forceinline__ void ts_unit_tile(const GemmParams& p, long long u, i
 
 // TA / TB: op(A) = A^T (A stored k x m, k contiguous) / op(B) = B^T (B stored n x k):
 // only the TMA boxes and the splitters' shared-memory reads change (NEXT row 2)
-template <int MODE, bool RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false>
+// RANGE: the FP16 overflow flag (p.range_flag) and the range-safe mode's power-of-two
+// scaling (p.row_max / p.col_max, R#22) are compiled in, each still enabled by its pointer.
+// MC: epilogue stores every tile to p.dst[0 .. num_dst-1] (fused all-gather, NEXT row 3)
+template <int MODE, bool RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false, bool MC = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, SPLITC_, ASTAT_>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
@@ -228,76 +231,101 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 PROF_ADD(P_MMA_WAIT_ACC);
                                 TRACE_AT(1, 5, kb);
                                 ptx::tc_fence_after();
-                                // a k-block longer than the operand ring (kb_stages > SOP) is
-                                // issued in chunks of <= SOP stages: P2 + P3 of a chunk, then its
-                                // P1 (which frees the chunk's slots); D_corr is committed before
-                                // the last chunk's P1, so its drain still overlaps P1.  Each
-                                // accumulator sees its stages in ascending order either way.
-                                for (int c0 = ks0; c0 < ks1; c0 += Cfg::SOP) {
-                                    const int c1 = min(c0 + Cfg::SOP, ks1);
+                                // P2 + P3 of stage ks (operand slot s) into D_corr; P1 into D_hi
+                                auto issue_corr = [&](int ks, uint32_t s) {
+                                    if (!p.corr) return;
+                                    const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
+                                    const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
+                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                                    for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                        const uint64_t dB_hi =
+                                            ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint64_t dB_lo =
+                                            ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint32_t ka = st * Cfg::KCOLS;
+                                        const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                        if (MODE == 0) {
+                                            ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);   // P2
+                                            ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);    // P3
+                                        } else {
+                                            ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
+                                            ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
+                                        }
+                                    }
+                                };
+                                auto issue_hi = [&](int ks, uint32_t s) {
+                                    const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
+                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+#pragma unroll
+                                    for (int st = 0; st < Cfg::NSTEPS; ++st) {
+                                        const uint64_t dB_hi =
+                                            ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
+                                        if (MODE == 0)
+                                            ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
+                                        else
+                                            ptx::mma_tf32_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);
+                                    }
+                                    ptx::tc_commit_pair(&op_empty[s], 0x3);   // B (and non-stationary A) slot free
+                                    if (lastA) ptx::tc_commit_pair(&aslot_empty[ks], 0x3);
+                                };
+                                if (ks1 - ks0 <= Cfg::SOP) {
+                                    // the whole k-block fits the operand ring: P2 + P3 of every
+                                    // stage, commit D_corr (its drain overlaps P1), then P1
                                     uint32_t s = s0, ph = ph0;
-                                    for (int ks = c0; ks < c1; ++ks) {
+                                    for (int ks = ks0; ks < ks1; ++ks) {
                                         PROF_T0();
                                         ptx::mbar_wait(&op_full[s], ph);
                                         PROF_ADD(P_MMA_WAIT_OP);
                                         TRACE_AT(1, 9, ks);
                                         ptx::tc_fence_after();
                                         PROF_T0();
-                                        if (p.corr) {
-                                            const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
-                                            const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
-                                            const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
-#pragma unroll
-                                            for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                                const uint64_t dB_hi =
-                                                    ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                                const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32,
-                                                                                      16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                                const uint32_t ka = st * Cfg::KCOLS;
-                                                const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
-                                                if (MODE == 0) {
-                                                    ptx::mma_f16_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);   // P2
-                                                    ptx::mma_f16_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);    // P3
-                                                } else {
-                                                    ptx::mma_tf32_pair_ts(d_corr, a_lo + ka, dB_hi, idesc, acc);
-                                                    ptx::mma_tf32_pair_ts(d_corr, a_hi + ka, dB_lo, idesc, 1u);
-                                                }
-                                            }
-                                        }
+                                        issue_corr(ks, s);
                                         PROF_ADD(P_MMA_ISSUE);
                                         if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                                     }
-                                    if (c1 == ks1) {
-                                        ptx::tc_commit_pair(&acc_full[1], 0x3);
-                                        TRACE_AT(1, 6, kb);
-                                    }
-                                    if (c0 == ks0) {
-                                        PROF_T0();
-                                        ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
-                                        PROF_ADD(P_MMA_WAIT_ACC);
-                                        TRACE_AT(1, 7, kb);
-                                        ptx::tc_fence_after();
-                                    }
+                                    ptx::tc_commit_pair(&acc_full[1], 0x3);
+                                    TRACE_AT(1, 6, kb);
+                                    PROF_T0();
+                                    ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
+                                    PROF_ADD(P_MMA_WAIT_ACC);
+                                    TRACE_AT(1, 7, kb);
+                                    ptx::tc_fence_after();
                                     PROF_T0();
                                     s = s0; ph = ph0;
-                                    for (int ks = c0; ks < c1; ++ks) {
-                                        const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
-                                        const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
-#pragma unroll
-                                        for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                            const uint64_t dB_hi =
-                                                ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                            const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
-                                            if (MODE == 0)
-                                                ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
-                                            else
-                                                ptx::mma_tf32_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);
-                                        }
-                                        ptx::tc_commit_pair(&op_empty[s], 0x3);   // B (and non-stationary A) slot free
-                                        if (lastA) ptx::tc_commit_pair(&aslot_empty[ks], 0x3);
+                                    for (int ks = ks0; ks < ks1; ++ks) {
+                                        issue_hi(ks, s);
                                         if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
                                     }
                                     s0 = s; ph0 = ph;
+                                } else {
+                                    // a k-block longer than the operand ring is issued in chunks of
+                                    // <= SOP stages: P2 + P3 of a chunk, then its P1 (which frees the
+                                    // chunk's slots); D_corr is committed before the last chunk's P1,
+                                    // so its drain still overlaps P1.  Each accumulator sees its
+                                    // stages in ascending order either way.
+                                    for (int c0 = ks0; c0 < ks1; c0 += Cfg::SOP) {
+                                        const int c1 = min(c0 + Cfg::SOP, ks1);
+                                        uint32_t s = s0, ph = ph0;
+                                        for (int ks = c0; ks < c1; ++ks) {
+                                            ptx::mbar_wait(&op_full[s], ph);
+                                            ptx::tc_fence_after();
+                                            issue_corr(ks, s);
+                                            if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                                        }
+                                        if (c1 == ks1) ptx::tc_commit_pair(&acc_full[1], 0x3);
+                                        if (c0 == ks0) {
+                                            ptx::mbar_wait(&acc_empty[0], aph ^ 1u);
+                                            ptx::tc_fence_after();
+                                        }
+                                        s = s0; ph = ph0;
+                                        for (int ks = c0; ks < c1; ++ks) {
+                                            issue_hi(ks, s);
+                                            if (++s == Cfg::SOP) { s = 0; ph ^= 1; }
+                                        }
+                                        s0 = s; ph0 = ph;
+                                    }
                                 }
                                 ptx::tc_commit_pair(&acc_full[0], 0x3);
                                 PROF_ADD(P_MMA_ISSUE);
@@ -376,7 +404,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 const bool doA = !ASTAT || j == 0;
                 // range-safe mode: this thread's row of A and column of B scale by 2^-e
                 float sa = 1.0f, sb = 1.0f;
-                if (p.row_max) {
+                if (RANGE && p.row_max) {
                     int b, mt, nt;
                     ts_unit_tile<ASTAT>(p, u, j, b, mt, nt);
                     const int r = mt * 256 + (int)rank * Cfg::BM + (int)m;
@@ -432,7 +460,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         for (int c = 0; c < 2; ++c)
                             vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
                     }
-                    if (p.row_max) {   // exact power-of-two scaling (RN where the result is subnormal)
+                    if (RANGE && p.row_max) {   // exact power-of-two scaling (RN where the result is subnormal)
                         if (doA) {
 #pragma unroll
                             for (int jj = 0; jj < Cfg::KS; ++jj) av[jj] = __fmul_rn(av[jj], sa);
@@ -511,7 +539,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 }
             }
         }
-        if (RANGE) {
+        if (RANGE && p.range_flag) {
             nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
             if (nonfinite && lane == 0) atomicOr(p.range_flag, 1u);
         }
@@ -634,7 +662,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 PROF_T0();
                 if (lane == 0) TRACE_AT(3 + e, 14, j);
                 const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
-                if (p.row_max) {   // range-safe mode: C_acc * 2^f_j * 2^e_i (exact unless out of range)
+                if (RANGE && p.row_max) {   // range-safe mode: C_acc * 2^f_j * 2^e_i (exact unless out of range)
                     const int r = mrow0 + (int)(q * 32 + lane);
                     const float ua = r < p.m ? pow2i(range_exp_of(p.row_max[(long long)b * p.m + r])) : 1.0f;
                     const int colb = nt * Cfg::BN + (int)(h * HALF);
@@ -677,11 +705,13 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 if (col0 + jj < p.n) cp[(long long)jj * p.ldc] = fmaf(p.alpha, creg[jj], 0.0f);
                             // fused all-gather (NEXT row 3): the same tile to every other
                             // destination -- peer C buffers over NVLink on a multi-GPU run
-                            for (int d = 1; d < p.num_dst; ++d) {
-                                float* dp = p.dst[d] + r + (long long)col0 * p.ldc;
+                            if constexpr (MC) {
+                                for (int d = 1; d < p.num_dst; ++d) {
+                                    float* dp = p.dst[d] + r + (long long)col0 * p.ldc;
 #pragma unroll
-                                for (int jj = 0; jj < HALF; ++jj)
-                                    if (col0 + jj < p.n) dp[(long long)jj * p.ldc] = fmaf(p.alpha, creg[jj], 0.0f);
+                                    for (int jj = 0; jj < HALF; ++jj)
+                                        if (col0 + jj < p.n) dp[(long long)jj * p.ldc] = fmaf(p.alpha, creg[jj], 0.0f);
+                                }
                             }
                         }
                     }

@@ -1,7 +1,7 @@
 """Interleaved A/B of two builds of libemusgemm.so on c2 (1024 x 256^3) and c3
 (16384^3): the same inputs and launch, alternating libraries, CUDA-event timing.
 
-    python tools/ab_lib.py LIB_A LIB_B [rounds]
+    python tools/ab_lib.py LIB_A.so LIB_B.so [LIB_C.so ...] [rounds] [kblock]
 """
 import ctypes
 import json
@@ -38,24 +38,41 @@ def timed(L, batch, N, A, B, C, mode, kb, it):
     return 2.0 * batch * N ** 3 / ms / 1e9
 
 
+def clocks():
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        return (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                round(pynvml.nvmlDeviceGetPowerUsage(h) / 1000))
+    except Exception:
+        return (None, None)
+
+
 def main():
-    libs = {"A": load(sys.argv[1]), "B": load(sys.argv[2])}
-    rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    paths = [a for a in sys.argv[1:] if a.endswith(".so")]
+    rest = [a for a in sys.argv[1:] if not a.endswith(".so")]
+    names = [chr(ord("A") + i) for i in range(len(paths))]
+    libs = {nm: load(pth) for nm, pth in zip(names, paths)}
+    rounds = int(rest[0]) if len(rest) > 0 else 3
+    kb = int(rest[1]) if len(rest) > 1 else 64
     res = {}
-    for shape, (batch, N, it) in {"c2": (1024, 256, 100), "c3": (1, 16384, 3)}.items():
+    # ABBA order per round so that drift over time favours neither library
+    for shape, (batch, N, it) in {"c2": (1024, 256, 1000), "c3": (1, 16384, 5)}.items():
         A = torch.rand(batch, N, N, device="cuda") * 2 - 1
         B = torch.rand(batch, N, N, device="cuda") * 2 - 1
         C = torch.empty(batch, N, N, device="cuda")
         for r in range(rounds):
             for mode in (0, 1):
-                if shape == "c3" and mode == 1 and r > 0:
-                    continue
-                for name, L in libs.items():
+                for name in names + names[::-1]:
                     key = f"{shape}_{'fp16' if mode == 0 else 'tf32'}_{name}"
-                    res.setdefault(key, []).append(round(timed(L, batch, N, A, B, C, mode, 64, it), 1))
+                    tf = round(timed(libs[name], batch, N, A, B, C, mode, kb, it), 1)
+                    res.setdefault(key, []).append(tf)
+                    res.setdefault(key + "_clk_pow", []).append(clocks())
         del A, B, C
         torch.cuda.empty_cache()
-    print(json.dumps(res), flush=True)
+    summary = {k: round(sum(v) / len(v), 1) for k, v in res.items() if not k.endswith("_clk_pow")}
+    print(json.dumps({"libs": dict(zip(names, paths)), "mean": summary, "all": res}), flush=True)
 
 
 if __name__ == "__main__":
