@@ -8,7 +8,7 @@ import pytest
 
 import oracle
 import workloads
-from gpu_util import emu_gpu, emu_gpu_range, tolerance
+from gpu_util import assert_bits_equal, emu_gpu, emu_gpu_range, tolerance
 
 pytestmark = pytest.mark.gpu
 MODES = ["fp16", "tf32"]
@@ -25,6 +25,10 @@ def _cmp(mode, A, B, m, n, k, kblock=0, **kw):
     d = np.abs(C.astype(np.float64) - ref.astype(np.float64))
     ratio = np.max(d / np.where(tol > 0, tol, 1.0))
     assert np.all(d <= tol), f"max |gpu-oracle|/tol = {ratio:.3g}"
+    # bit for bit with the measured tensor-core model (R#9)
+    hw = oracle.emu_gemm_range(mode, A, B, m, n, k, kb=kb, alpha=kw.get("alpha", 1.0), beta=kw.get("beta", 0.0),
+                               C=kw.get("C"), corr=not (kw.get("flags", 0) & 1), tc="sm100")
+    assert_bits_equal(C, hw)
     return C, ref
 
 

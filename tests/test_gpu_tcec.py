@@ -143,6 +143,7 @@ def test_householder_generated_operand(mode, m):
         ref = oracle.emu_gemm(mode, Hc, X[b:b + 1], m, n, m)
         tol = tolerance(mode, Hc, X[b:b + 1], m, n, m)
         assert np.all(np.abs(C[b:b + 1].astype(np.float64) - ref) <= tol), b
+        assert_bits_equal(C[b:b + 1], oracle.emu_gemm(mode, Hc, X[b:b + 1], m, n, m, tc="sm100"))
 
 
 def _givens(mode, m, n, i, j, CS, X, flags=0):
@@ -173,6 +174,7 @@ def test_givens_map_operand(mode, mij):
         Gc = workloads.colmajor(structured.givens_matrix(m, i, j, *CS[b]))[None]
         ref = oracle.emu_gemm(mode, Gc, X[b:b + 1], m, n, m)
         assert np.all(np.abs(C[b:b + 1].astype(np.float64) - ref) <= tolerance(mode, Gc, X[b:b + 1], m, n, m))
+        assert_bits_equal(C[b:b + 1], oracle.emu_gemm(mode, Gc, X[b:b + 1], m, n, m, tc="sm100"))
 
 
 def _scan(mode, n, count, X, flags=0):
@@ -195,6 +197,7 @@ def test_scan_generated_operand(mode, n):
     Lc = workloads.colmajor(structured.scan_matrix(n))[None]
     ref = oracle.emu_gemm(mode, Lc, X[None], n, count, n)[0]
     assert np.all(np.abs(Y.astype(np.float64) - ref) <= tolerance(mode, Lc, X[None], n, count, n)[0])
+    assert_bits_equal(Y, oracle.emu_gemm(mode, Lc, X[None], n, count, n, tc="sm100")[0])
 
 
 def test_tcec_argument_errors():
