@@ -15,4 +15,11 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 5 -c 10
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:emu_sgemm -s 3 -c 1 -o gpurun_out/prof_c2_fp16_$TAG python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:emu_sgemm -s 3 -c 1 -o gpurun_out/prof_c2_tf32_$TAG python bench.py --mode tf32 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:emu_sgemm -s 3 -c 1 -o gpurun_out/prof_c3_fp16_$TAG python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+# raw-page exports travel back; the full reports only while gpurun_out stays under its 64 MiB cap
+for r in gpurun_out/prof_*_$TAG.ncu-rep; do ncu -i $r --page raw --csv > ${r%.ncu-rep}.raw.csv 2>/dev/null; done
+for r in gpurun_out/prof_c2_tf32_$TAG.ncu-rep gpurun_out/prof_c3_fp16_$TAG.ncu-rep; do
+  [ $(du -sm gpurun_out | cut -f1) -gt 48 ] && rm -f $r
+done
+rm -f gpurun_out/tc_samples.npz
+du -sh gpurun_out
 echo done

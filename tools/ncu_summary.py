@@ -19,7 +19,12 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg", "dram__bytes_read.su
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep, or the `ncu -i REP --page raw --csv` export of one (.csv)"""
+    if rep.endswith(".csv"):
+        with open(rep) as f:
+            out = f.read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, u, v = rows[0], rows[1], rows[2]
     d = {"Kernel Name": v[h.index("Kernel Name")]}

@@ -24,7 +24,10 @@ def val(s):
 def main():
     tag = sys.argv[1]
     out = os.path.join(ROOT, "gpurun_out")
-    reps = {c: os.path.join(out, f"prof_{c}_{tag}.ncu-rep") for c in ("c2_fp16", "c2_tf32", "c3_fp16")}
+    reps = {}
+    for c in ("c2_fp16", "c2_tf32", "c3_fp16"):
+        rep = os.path.join(out, f"prof_{c}_{tag}.ncu-rep")
+        reps[c] = rep if os.path.exists(rep) else os.path.join(out, f"prof_{c}_{tag}.raw.csv")
     summ, traffic = {}, {}
     for c, rep in reps.items():
         if not os.path.exists(rep):
