@@ -53,7 +53,7 @@ struct DeviceInfo {
     int sms = 0;
     bool attr_set[32] = {};
     bool pair_attr_set[16] = {};
-    bool ts_attr_set[128] = {};
+    bool ts_attr_set[256] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -365,7 +365,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT>;
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        const int slot = (((((MODE * 2 + (RANGE ? 1 : 0)) * 2 + (BN == 96 ? 0 : 1)) * 2 + (SPLITC ? 1 : 0)) * 2 +
+        const int slot = (((((MODE * 2 + (RANGE ? 1 : 0)) * 3 + (BN == 96 ? 0 : BN == 128 ? 1 : 2)) * 2 + (SPLITC ? 1 : 0)) * 2 +
                            (ASTAT ? 1 : 0)) * 2 + (TA ? 1 : 0)) * 2 + (TB ? 1 : 0);
         if (!g_dev[dev].ts_attr_set[slot]) {
             if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>,
@@ -584,7 +584,10 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     // double-buffered 96-wide tile (EMU_TS_N=96) and the plain single buffer
     // (EMU_TS_SPLITC=0) stay selectable for comparison.
     static const int ts_n_env = env_int("EMU_TS_N", 0, 0, 128);   // tuning only
-    const int ts_n = ts_n_env ? ts_n_env : 128;
+    // few tiles (fewer 256 x 128 tiles than clusters, e.g. c4's 1024^2 output): 64-wide
+    // tiles with double-buffered accumulators put twice as many clusters to work
+    const long long ts_tiles128 = (long long)((m + 255) / 256) * ((n + 127) / 128) * batch;
+    const int ts_n = ts_n_env ? ts_n_env : (ts_tiles128 < sms / 2 && n > 64 && !g_mdst ? 64 : 128);
     static const int ts_sc_env = env_int("EMU_TS_SPLITC", 1, 0, 1);   // tuning only (default on)
     static const int ts_as_env = env_int("EMU_TS_ASTAT", 1, 0, 1);    // tuning only (default on)
     const bool ts_sc = ts_n == 128 && ts_sc_env;
@@ -603,6 +606,10 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
                                                                     d_range_flag, kblock, flags, row_max, col_max); break; }    \
         if (ts_sc)                                                                                                     \
             { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,     \
+                                                                     ldb, strideB, beta, C, ldc, strideC, batch, s,    \
+                                                                     d_range_flag, kblock, flags, row_max, col_max); break; }   \
+        if (ts_n == 64)                                                                                                \
+            { rs = run_gemm_pair_ts<MODE_, RANGE_, 64, false, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,     \
                                                                      ldb, strideB, beta, C, ldc, strideC, batch, s,    \
                                                                      d_range_flag, kblock, flags, row_max, col_max); break; }   \
         if (ts_n == 128)                                                                                               \

@@ -121,3 +121,30 @@ def test_default_kblock_rule(mode):
     C = emu_gpu(mode, A, B, m, n, k)
     assert np.array_equal(C, emu_gpu(mode, A, B, m, n, k, kblock=128))
     assert_bits_equal(C, oracle.emu_gemm(mode, A, B, m, n, k, tc="sm100"))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_few_tiles_64_wide(mode):
+    """fewer 256 x 128 tiles than clusters -> 64-wide tiles with double-buffered
+    accumulators (c4's 1024^2 output); same bits as the oracle"""
+    m, n, k = 384, 200, 500
+    A, B = workloads.make_operands(1, m, n, k, seed=970)
+    _check(mode, A, B, m, n, k)
+    m, n, k = 1024, 1024, 4096        # c4's shape, sampled outputs
+    A, B = workloads.make_operands(1, m, n, k, seed=971)
+    C = emu_gpu(mode, A, B, m, n, k)
+    g = workloads.rng(972)
+    i, j = g.integers(0, m, 256), g.integers(0, n, 256)
+    b = np.zeros(256, dtype=np.int64)
+    assert_bits_equal(C[0, j, i], oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="sm100"))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_streaming_128_wide(mode):
+    """enough tiles for every cluster but too few row blocks for A-stationary:
+    the streaming-A split-commit 128-wide kernel"""
+    batch, m, n, k = 40, 256, 256, 300
+    A, B = workloads.make_operands(batch, m, n, k, seed=980)
+    C = emu_gpu(mode, A, B, m, n, k)
+    items = [0, 17, 39]
+    assert_bits_equal(C[items], oracle.emu_gemm(mode, A[items], B[items], m, n, k, tc="sm100"))
