@@ -148,3 +148,29 @@ def test_streaming_128_wide(mode):
     C = emu_gpu(mode, A, B, m, n, k)
     items = [0, 17, 39]
     assert_bits_equal(C[items], oracle.emu_gemm(mode, A[items], B[items], m, n, k, tc="sm100"))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c1_full(mode):
+    """BASELINE.json configs[0]: 16 x 64^3 (single-CTA kernel), every output"""
+    A, B = workloads.make_operands(16, 64, 64, 64, seed=42)
+    _check(mode, A, B, 64, 64, 64)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c5_full_size_sampled(mode):
+    """BASELINE.json configs[4]: 8192 x 256^3 in one launch (the 1-GPU share of the
+    batch-sharded run); sampled outputs across the whole batch"""
+    import torch
+    import paper_2308_15152_b200 as emu
+    batch, m, n, k = 8192, 256, 256, 256
+    A, B = workloads.make_operands(batch, m, n, k, seed=5)
+    dC = torch.empty((batch, n, m), device="cuda")
+    emu.emu_sgemm_batched(m, n, k, 1.0, torch.from_numpy(A).cuda(), m, k * m, torch.from_numpy(B).cuda(), k,
+                          n * k, 0.0, dC, m, n * m, batch, mode)
+    torch.cuda.synchronize()
+    g = workloads.rng(6)
+    b, i, j = g.integers(0, batch, 512), g.integers(0, m, 512), g.integers(0, n, 512)
+    b[0], i[0], j[0] = batch - 1, m - 1, n - 1
+    got = dC[torch.from_numpy(b), torch.from_numpy(j), torch.from_numpy(i)].cpu().numpy()
+    assert_bits_equal(got, oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="sm100"))
