@@ -179,6 +179,14 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             // -------------------------------------------- TMA producer (both CTAs)
             if (ptx::elect_one()) {
                 uint32_t s = 0, ph = 0;
+                // L2 hints (tuning, EMU_L2_POLICY): bit 0 -> B evict_first, bit 1 -> A evict_last
+                const uint64_t pol_a = ptx::l2_policy_evict_last(), pol_b = ptx::l2_policy_evict_first();
+                auto load = [&](uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, bool hint,
+                                uint64_t pol) {
+                    if (hint) ptx::tma_load_3d(dst, map, bar, c0, c1, c2, pol);
+                    else ptx::tma_load_3d_nohint(dst, map, bar, c0, c1, c2);
+                };
+                const bool hint_a = (p.l2_policy & 2) != 0, hint_b = (p.l2_policy & 1) != 0;
                 for (long long u = cid; u < num_units; u += ncl) {
                     for (int j = 0; j < R; ++j) {
                         int b, mt, nt;
@@ -194,18 +202,18 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                             ptx::mbar_arrive_expect_tx(&f32_full[s], loadA ? Cfg::F32_STAGE : Cfg::B32_BYTES);
                             if (loadA) {
                                 if (TA)   // [128 m][32 k], SWIZZLE_128B rows
-                                    ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], ks * Cfg::BK,
-                                                            mt * 256 + rank * Cfg::BM, ab);
+                                    load(dst, &tmA, &f32_full[s], ks * Cfg::BK, mt * 256 + rank * Cfg::BM, ab,
+                                         hint_a, pol_a);
                                 else      // [32 k][128 m]
-                                    ptx::tma_load_3d_nohint(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM,
-                                                            ks * Cfg::BK, ab);
+                                    load(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab,
+                                         hint_a, pol_a);
                             }
                             if (TB)       // [32 k][BN/2 n]
-                                ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s],
-                                                        nt * Cfg::BN + rank * Cfg::BNC, ks * Cfg::BK, bb);
+                                load(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], nt * Cfg::BN + rank * Cfg::BNC,
+                                     ks * Cfg::BK, bb, hint_b, pol_b);
                             else          // [BN/2 n][32 k], SWIZZLE_128B rows
-                                ptx::tma_load_3d_nohint(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
-                                                        nt * Cfg::BN + rank * Cfg::BNC, bb);
+                                load(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], ks * Cfg::BK,
+                                     nt * Cfg::BN + rank * Cfg::BNC, bb, hint_b, pol_b);
                             if (++s == Cfg::S32) { s = 0; ph ^= 1; }
                         }
                     }

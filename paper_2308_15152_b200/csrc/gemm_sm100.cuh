@@ -109,7 +109,8 @@ struct GemmParams {
     int tma_store;                // 1: epilogue stages C in shared memory and TMA-stores it (beta == 0)
     int prefetch;                 // L2 prefetch distance in k-stages (0 = off)
     int group_m;                  // raster: m-tiles per group walking the n-tiles together
-    int l2_policy;                // 0 default; 1 B evict_last; 2 A evict_last; 3 both
+    int l2_policy;                // 0 default; bit 1: A evict_last; bit 0: B evict_last
+                                  // (TS kernel: B evict_first)
     unsigned int* range_flag;     // nullable (FP16 mode only)
     // range-safe mode (TS kernel): max |x| bit patterns of the rows of A / columns of
     // B, [batch][m] and [batch][n]; nullptr = unscaled (the paper's method)
