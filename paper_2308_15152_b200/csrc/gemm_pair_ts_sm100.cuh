@@ -91,6 +91,7 @@ struct PairTsCfg {
     static_assert(SMEM_BYTES <= 232448, "shared memory");
     static_assert(SOP >= 2, "TMEM budget for A stages");
     static_assert(ECOLS % 8 == 0, "combine columns");
+    static_assert(!SPLITC || ECOLS % 16 == 0, "split-commit combine drains 16-column chunks");
 };
 
 // tile j of work unit u: A-stationary -> n-tile j of (batch, m-pair) row block u;
@@ -580,10 +581,10 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         if (lane == 0) TRACE_AT(3 + e, 10, kb);
                         PROF_T0();
                         ptx::tc_fence_after();
-                        float vc[HALF / 8][8];
+                        float vc[HALF / 16][16];   // x16 loads: fewer instructions on the drain
                         if (p.corr) {
 #pragma unroll
-                            for (int c = 0; c < HALF / 8; ++c) ptx::tmem_ld8(taddr + Cfg::BN + c * 8, vc[c]);
+                            for (int c = 0; c < HALF / 16; ++c) ptx::tmem_ld16(taddr + Cfg::BN + c * 16, vc[c]);
                             ptx::tmem_wait_ld();
                         }
                         ptx::tc_fence_before();
@@ -597,31 +598,26 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         if (lane == 0) TRACE_AT(3 + e, 12, kb);
                         PROF_T0();
                         ptx::tc_fence_after();
-                        constexpr int CPW = 2;
 #pragma unroll
-                        for (int c0 = 0; c0 < HALF / 8; c0 += CPW) {
-                            float vh[CPW][8];
-#pragma unroll
-                            for (int c = 0; c < CPW; ++c) ptx::tmem_ld8(taddr + (c0 + c) * 8, vh[c]);
+                        for (int c0 = 0; c0 < HALF / 16; ++c0) {   // 16-column chunks of D_hi
+                            float vh[16];
+                            ptx::tmem_ld16(taddr + c0 * 16, vh);
                             ptx::tmem_wait_ld();
-                            if (c0 + CPW >= HALF / 8) {   // last chunk read: release D_hi before the math
+                            if (c0 + 1 == HALF / 16) {   // last chunk read: release D_hi before the math
                                 ptx::tc_fence_before();
                                 __syncwarp();
                                 if (lane == 0) ptx::mbar_arrive_cluster(emp_hi);
                                 if (lane == 0) TRACE_AT(3 + e, 13, kb);
                             }
+                            float* cr = creg + c0 * 16;
+                            const float* cc = vc[c0];
+                            if (p.corr) {
 #pragma unroll
-                            for (int c = 0; c < CPW; ++c) {
-                                float* cr = creg + (c0 + c) * 8;
-                                const float* cc = vc[c0 + c];
-                                if (p.corr) {
+                                for (int jj = 0; jj < 16; jj += 2)
+                                    combine2(cr[jj], cr[jj + 1], vh[jj], vh[jj + 1], cc[jj], cc[jj + 1], scale);
+                            } else {
 #pragma unroll
-                                    for (int jj = 0; jj < 8; jj += 2)
-                                        combine2(cr[jj], cr[jj + 1], vh[c][jj], vh[c][jj + 1], cc[jj], cc[jj + 1], scale);
-                                } else {
-#pragma unroll
-                                    for (int jj = 0; jj < 8; ++jj) cr[jj] = __fadd_rn(cr[jj], vh[c][jj]);
-                                }
+                                for (int jj = 0; jj < 16; ++jj) cr[jj] = __fadd_rn(cr[jj], vh[jj]);
                             }
                         }
                         PROF_ADD(P_EPI_DRAIN);

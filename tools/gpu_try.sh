@@ -11,4 +11,4 @@ timeout 1200 python tools/ab_lib.py "$@" paper_2308_15152_b200/libemusgemm.so 2 
 python -c "import json; d=json.load(open('gpurun_out/ab_$TAG.json')); print(json.dumps(d['libs'])); print(json.dumps(d['mean']))"
 timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_$TAG.log 2>&1
 tail -1 gpurun_out/bench_$TAG.log | cut -c1-200
-timeout 300 python tools/trace.py fp16 > gpurun_out/trace_$TAG.txt 2>&1; grep -A 20 "^intervals" gpurun_out/trace_$TAG.txt
+
