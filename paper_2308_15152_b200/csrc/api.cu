@@ -132,29 +132,34 @@ __global__ void scale_c_kernel(float* C, int m, int n, long long ldc, long long 
 
 // range-safe mode (R#22): bit patterns of the max finite |x| of every row of A_b and
 // column of B_b (non-negative binary32 values order like their bit patterns, so an
-// integer atomicMax merges the k-chunks).  blockIdx.x: (item, A row block of 256 | B
-// column block of 8 warps), blockIdx.y: k-chunk.
+// integer atomicMax merges the k-chunks).  One block per (item, A row block of 256 x
+// k-chunk of ka) or (item, B column block of 8 warps x k-chunk of kb): short A chunks
+// give the row pass (one strided column read per k) enough blocks to reach HBM rates.
 __global__ void range_max_kernel(const float* __restrict__ A, long long lda, long long strideA,
                                  const float* __restrict__ B, long long ldb, long long strideB, int m, int n, int k,
-                                 int a_blocks, int b_blocks, int kchunk, unsigned* __restrict__ row_max,
+                                 int a_blocks, int b_blocks, int ka, int kb, unsigned* __restrict__ row_max,
                                  unsigned* __restrict__ col_max)
 {
-    const int per_item = a_blocks + b_blocks;
+    const int a_ch = (k + ka - 1) / ka, b_ch = (k + kb - 1) / kb;
+    const long long per_item = (long long)a_blocks * a_ch + (long long)b_blocks * b_ch;
     const long long item = blockIdx.x / per_item;
-    const int blk = (int)(blockIdx.x - item * per_item);
-    const int p0 = blockIdx.y * kchunk, p1 = min(k, p0 + kchunk);
-    if (blk < a_blocks) {
+    long long w = blockIdx.x - item * per_item;
+    if (w < (long long)a_blocks * a_ch) {
+        const int blk = (int)(w / a_ch), p0 = (int)(w % a_ch) * ka, p1 = min(k, p0 + ka);
         const int r = blk * 256 + (int)threadIdx.x;
         if (r >= m) return;
         const float* a = A + item * strideA + r;
         float mx = 0.0f;
+#pragma unroll 8
         for (int p = p0; p < p1; ++p) {
             const float v = fabsf(__ldg(a + (long long)p * lda));
             if (v <= 3.402823466e38f) mx = fmaxf(mx, v);   // finite values only (NaN compares false)
         }
         if (mx > 0.0f) atomicMax(row_max + item * m + r, __float_as_uint(mx));
     } else {
-        const int c = (blk - a_blocks) * 8 + (int)(threadIdx.x >> 5);
+        w -= (long long)a_blocks * a_ch;
+        const int blk = (int)(w / b_ch), p0 = (int)(w % b_ch) * kb, p1 = min(k, p0 + kb);
+        const int c = blk * 8 + (int)(threadIdx.x >> 5);
         if (c >= n) return;
         const float* bcol = B + item * strideB + (long long)c * ldb;
         float mx = 0.0f;
@@ -559,11 +564,14 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
         unsigned* ws = static_cast<unsigned*>(range_ws);
         if (cudaMemsetAsync(ws, 0, (size_t)4 * batch * ((size_t)m + n), s) != cudaSuccess)
             return EMU_STATUS_CUDA_ERROR;
-        const int a_blocks = (m + 255) / 256, b_blocks = (n + 7) / 8, kchunk = 512;
-        const dim3 grid((unsigned)((long long)batch * (a_blocks + b_blocks)), (unsigned)((k + kchunk - 1) / kchunk));
+        const int a_blocks = (m + 255) / 256, b_blocks = (n + 7) / 8, ka = 16, kb = 512;
+        const long long blocks = (long long)batch * ((long long)a_blocks * ((k + ka - 1) / ka) +
+                                                     (long long)b_blocks * ((k + kb - 1) / kb));
+        if (blocks > 0x7fffffffLL) return EMU_STATUS_NOT_SUPPORTED;
         const long long sAr = batch > 1 ? strideA : 0, sBr = batch > 1 ? strideB : 0;
-        range_max_kernel<<<grid, 256, 0, s>>>(A, lda, sAr, B, ldb, sBr, m, n, k, a_blocks, b_blocks, kchunk, ws,
-                                              ws + (size_t)batch * m);
+        if (blocks > 0)
+            range_max_kernel<<<(unsigned)blocks, 256, 0, s>>>(A, lda, sAr, B, ldb, sBr, m, n, k, a_blocks, b_blocks,
+                                                               ka, kb, ws, ws + (size_t)batch * m);
         const emu_status ls = launch_status(cudaGetLastError());
         if (ls != EMU_STATUS_SUCCESS) return ls;
         row_max = ws;

@@ -408,6 +408,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t tq = tmem_base + ((q * 32u) << 16);
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0, unit_it = 0;
         uint32_t nonfinite = 0;
+        const bool chk = RANGE && p.range_flag != nullptr;   // the FP16 overflow flag was asked for
         for (long long u = cid; u < num_units; u += ncl, ++unit_it) {
             for (int j = 0; j < R; ++j) {
                 const bool doA = !ASTAT || j == 0;
@@ -491,7 +492,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll
                             for (int jj = 0; jj < Cfg::KS / 2; ++jj) {
                                 split_fp16x2(av[2 * jj], av[2 * jj + 1], h[jj], l[jj]);
-                                if (RANGE) nonfinite |= f16x2_nonfinite(h[jj]);
+                                if (chk) nonfinite |= f16x2_nonfinite(h[jj]);
                             }
                             ptx::tmem_st8(a_hi + kq * (Cfg::KS / 2), h);
                             ptx::tmem_st8(a_lo + kq * (Cfg::KS / 2), l);
@@ -513,7 +514,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         uint2 h0, l0, h1, l1;
                         split4_fp16(vb[0], h0, l0);
                         split4_fp16(vb[1], h1, l1);
-                        if (RANGE)
+                        if (chk)
                             nonfinite |= f16x2_nonfinite(h0.x) | f16x2_nonfinite(h0.y) | f16x2_nonfinite(h1.x) |
                                          f16x2_nonfinite(h1.y);
                         const uint32_t off = n * 64 + ((quarter ^ ((n >> 1) & 3)) << 4);
