@@ -633,6 +633,25 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         PROF_T0();
                         ptx::tc_fence_after();
                         const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * 2 * Cfg::BN + h * HALF;
+                        if constexpr (HALF % 16 == 0) {
+                            // x16 loads: one instruction per 16 columns of each part
+#pragma unroll
+                            for (int c0 = 0; c0 < HALF / 16; ++c0) {
+                                float vh[16], vc[16];
+                                ptx::tmem_ld16(taddr + c0 * 16, vh);
+                                ptx::tmem_ld16(taddr + Cfg::BN + c0 * 16, vc);
+                                ptx::tmem_wait_ld();
+                                float* cr = creg + c0 * 16;
+                                if (p.corr) {
+#pragma unroll
+                                    for (int jj = 0; jj < 16; jj += 2)
+                                        combine2(cr[jj], cr[jj + 1], vh[jj], vh[jj + 1], vc[jj], vc[jj + 1], scale);
+                                } else {
+#pragma unroll
+                                    for (int jj = 0; jj < 16; ++jj) cr[jj] = __fadd_rn(cr[jj], vh[jj]);
+                                }
+                            }
+                        } else {
                         // columns in chunks of 8; CPW chunks loaded per tcgen05.wait::ld
                         constexpr int NCH = HALF / 8, CPW = (HALF <= 24) ? NCH : 2;
 #pragma unroll
@@ -657,6 +676,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                     for (int jj = 0; jj < 8; ++jj) cr[jj] = __fadd_rn(cr[jj], vh[c][jj]);
                                 }
                             }
+                        }
                         }
                         ptx::tc_fence_before();
                         __syncwarp();
