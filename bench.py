@@ -47,6 +47,38 @@ def shard(rank: int, world: int, batch_per_rank: int):
     return rank * batch_per_rank, (rank + 1) * batch_per_rank
 
 
+def item_checksums(C):
+    """per-problem 64-bit checksums of the result bits: C is a
+    (batch, n, m) float32 tensor; sum over elements of bits * (index + 1), wrapping
+    mod 2^64, so a changed bit or a permuted element changes it"""
+    import torch
+    bits = C.contiguous().view(torch.int32).to(torch.int64).reshape(C.shape[0], -1)
+    w = torch.arange(1, bits.shape[1] + 1, device=C.device, dtype=torch.int64)
+    return (bits * w).sum(dim=1)
+
+
+def cross_rank_check(local_sums, batch, recompute, items=None):
+    """Multi-GPU verification outside the timed region: every rank's
+    per-problem checksums are gathered to rank 0, which recomputes the first and last
+    problem of every rank's shard by itself (`recompute(global_item)` -> checksum,
+    the single-GPU computation of that one problem) and compares bit for bit.
+    Returns the report on rank 0 (None elsewhere, {} without a process group)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return {}
+    world, rank = dist.get_world_size(), dist.get_rank()
+    gathered = torch.empty(world * batch, dtype=torch.int64, device=local_sums.device)
+    dist.all_gather_into_tensor(gathered, local_sums)
+    if rank != 0:
+        return None
+    items = items if items is not None else sorted({i for r in range(world) for i in (r * batch, r * batch + batch - 1)})
+    bad = [g for g in items if int(recompute(g)) != int(gathered[g])]
+    return {"items_checked": len(items), "bit_identical": not bad, "mismatched_items": bad[:8],
+            "method": "per-problem 64-bit checksums of C gathered over NCCL; rank 0 recomputes the first and "
+                      "last problem of every shard on its own GPU"}
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """max of a per-rank timing over all ranks (identity without a process group)."""
     import torch
@@ -401,6 +433,19 @@ def main():
     value = flops_step * args.steps / (ms_max / 1e3) / 1e12
     ms_per_step = ms_max / args.steps
 
+    # multi-GPU: every shard bit-identical to the single-GPU computation (outside timing)
+    def recompute(g):
+        A1, B1 = workloads.make_operands(1, m, n, k, cfg.seed, dist=cfg.dist, item0=g)
+        C1 = torch.empty((1, n, m), device="cuda")
+        a1, b1 = torch.from_numpy(A1).cuda(), torch.from_numpy(B1).cuda()
+        if use_range:
+            emu.emu_sgemm_batched_range(m, n, k, 1.0, a1, m, sA, b1, k, sB, 0.0, C1, m, sC, 1, mode, ws, ws_bytes)
+        else:
+            emu.emu_sgemm_batched(m, n, k, 1.0, a1, m, sA, b1, k, sB, 0.0, C1, m, sC, 1, mode)
+        torch.cuda.synchronize()
+        return item_checksums(C1)[0]
+    multi_check = cross_rank_check(item_checksums(dC), batch, recompute) if world > 1 else {}
+
     # accuracy on sampled problems of this rank (outside the timed region)
     import oracle
     idx = [0, batch // 2, batch - 1] if batch > 1 else [0]
@@ -486,6 +531,8 @@ def main():
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "paper_context": PAPER_A100,
     }
+    if world > 1:
+        out["multi_gpu_check"] = multi_check
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -73,3 +73,61 @@ def test_shard_ranges_tile_the_batch():
 
 def test_max_over_ranks_without_process_group():
     assert bench.max_over_ranks(3.5) == 3.5
+
+
+def _check_worker(rank, world, port, out, corrupt):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        per, m, n, k = 3, 16, 12, 20
+
+        def compute(items):
+            A, B = workloads.make_operands(len(items), m, n, k, seed=7, item0=items[0])
+            return torch.from_numpy(oracle.emu_gemm("fp16", A, B, m, n, k))
+
+        lo, hi = bench.shard(rank, world, per)
+        C = compute(list(range(lo, hi)))
+        if corrupt and rank == 1:
+            C[2, 3, 4] = float(np.nextafter(np.float32(C[2, 3, 4].item()), np.float32(np.inf)))
+        rep = bench.cross_rank_check(bench.item_checksums(C), per,
+                                     lambda g: bench.item_checksums(compute([g]))[0])
+        if rank == 0:
+            out.put(rep)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("corrupt", [False, True])
+def test_cross_rank_bit_identity_check_gloo(corrupt):
+    """bench.py's multi-GPU verification: gathered per-problem
+    checksums against rank 0's own recomputation; a one-ulp change in one output
+    of rank 1's last problem is caught"""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_check_worker, args=(r, world, port, q, corrupt)) for r in range(world)]
+    for p in procs:
+        p.start()
+    rep = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert rep["items_checked"] == 4
+    if corrupt:
+        assert not rep["bit_identical"] and rep["mismatched_items"] == [5]
+    else:
+        assert rep["bit_identical"]
+
+
+def test_item_checksums_detect_bit_changes():
+    C = torch.from_numpy(workloads.uniform((2, 8, 8), seed=3))
+    s0 = bench.item_checksums(C)
+    D = C.clone()
+    D[1, 2, 3] = float(np.nextafter(np.float32(D[1, 2, 3].item()), np.float32(0)))
+    s1 = bench.item_checksums(D)
+    assert s0[0] == s1[0] and s0[1] != s1[1]
+    E = C.clone()
+    E[0, 0, 0], E[0, 0, 1] = C[0, 0, 1], C[0, 0, 0]       # swapped elements
+    assert bench.item_checksums(E)[0] != s0[0] or C[0, 0, 0] == C[0, 0, 1]
