@@ -473,14 +473,12 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     if (RANGE && p.row_max) {   // exact power-of-two scaling (RN where the result is subnormal)
                         if (doA) {
 #pragma unroll
-                            for (int jj = 0; jj < Cfg::KS; ++jj) av[jj] = __fmul_rn(av[jj], sa);
+                            for (int jj = 0; jj < Cfg::KS; jj += 2) scale_f32x2(av[jj], av[jj + 1], sa);
                         }
 #pragma unroll
                         for (int c = 0; c < 2; ++c) {
-                            vb[c].x = __fmul_rn(vb[c].x, sb);
-                            vb[c].y = __fmul_rn(vb[c].y, sb);
-                            vb[c].z = __fmul_rn(vb[c].z, sb);
-                            vb[c].w = __fmul_rn(vb[c].w, sb);
+                            scale_f32x2(vb[c].x, vb[c].y, sb);
+                            scale_f32x2(vb[c].z, vb[c].w, sb);
                         }
                     }
                     // ---- A: split into TMEM columns (lane = m)

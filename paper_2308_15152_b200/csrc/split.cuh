@@ -61,6 +61,17 @@ __device__ __forceinline__ void sub_f16x2_from_f32x2(uint32_t h, float x0, float
         : "=f"(r0), "=f"(r1) : "r"(h), "f"(x0), "f"(x1));
 }
 
+// r0 *= s, r1 *= s with one packed FMUL2 (each product rounded exactly like __fmul_rn)
+__device__ __forceinline__ void scale_f32x2(float& r0, float& r1, float s)
+{
+    asm("{\n\t.reg .b64 d, b;\n\t"
+        "mov.b64 d, {%0, %1};\n\t"
+        "mov.b64 b, {%2, %2};\n\t"
+        "mul.rn.f32x2 d, d, b;\n\t"
+        "mov.b64 {%0, %1}, d;\n\t}"
+        : "+f"(r0), "+f"(r1) : "f"(s));
+}
+
 __device__ __forceinline__ void mul2048_f32x2(float& r0, float& r1)
 {
     asm("{\n\t.reg .b64 d, b;\n\t"

@@ -38,5 +38,10 @@ for mode in ("fp16", "tf32"):
     us = t(lambda: emu.emu_sgemm_batched_range(m, n, k, 1.0, A, m, 0, B, k, 0, 0.0, C, m, 0, 1, mode, ws,
                                                ws.numel(), None, None, 0, 0))
     out[f"{mode}_range_us"] = round(us, 1)
+# the same GEMM on operands scaled by 2^14 (the range-safe mode's operand magnitudes)
+A2, B2 = A * 16384.0, B * 16384.0
+for mode in ("fp16", "tf32"):
+    us = t(lambda: emu.emu_sgemm_batched(m, n, k, 1.0, A2, m, 0, B2, k, 0, 0.0, C, m, 0, 1, mode))
+    out[f"{mode}_plain_scaled_inputs_us"] = round(us, 1)
 out["EMU_TS_N"] = os.environ.get("EMU_TS_N", "auto")
 print(json.dumps(out))
