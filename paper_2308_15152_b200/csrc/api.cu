@@ -53,7 +53,7 @@ struct DeviceInfo {
     int sms = 0;
     bool attr_set[32] = {};
     bool pair_attr_set[16] = {};
-    bool ts_attr_set[256] = {};
+    bool ts_attr_set[512] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -361,7 +361,7 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
-template <int MODE, bool RANGE, int BN, bool SPLITC, bool ASTAT, bool TA = false, bool TB = false>
+template <int MODE, int RANGE, int BN, bool SPLITC, bool ASTAT, bool TA = false, bool TB = false>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
@@ -370,7 +370,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT>;
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        const int slot = (((((MODE * 2 + (RANGE ? 1 : 0)) * 3 + (BN == 96 ? 0 : BN == 128 ? 1 : 2)) * 2 + (SPLITC ? 1 : 0)) * 2 +
+        const int slot = (((((MODE * 4 + RANGE) * 3 + (BN == 96 ? 0 : BN == 128 ? 1 : 2)) * 2 + (SPLITC ? 1 : 0)) * 2 +
                            (ASTAT ? 1 : 0)) * 2 + (TA ? 1 : 0)) * 2 + (TB ? 1 : 0);
         if (!g_dev[dev].ts_attr_set[slot]) {
             if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>,
@@ -653,25 +653,28 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     if (ta || tb) {   // op(A) / op(B) transposed (NEXT row 2): split-commit TS kernel, 128-wide tiles
         emu_status rs;
         if (mode == EMU_SPLIT_FP16) {
-            if (d_range_flag) EMU_RUN_T3(0, true);
-            else EMU_RUN_T3(0, false);
+            if (d_range_flag) EMU_RUN_T3(0, 1);
+            else EMU_RUN_T3(0, 0);
         } else {
-            EMU_RUN_T3(1, false);
+            EMU_RUN_T3(1, 0);
         }
         return rs;
     }
 #undef EMU_RUN_T3
 #undef EMU_RUN_TT
     if (ts) {
-        // RANGE instantiations carry the overflow flag and the range-safe scaling; the
-        // plain ones (the paper's method) carry neither
+        // RANGE mask: 1 = the overflow flag code, 2 = the range-safe scaling; the plain
+        // instantiations (the paper's method) carry neither
         emu_status rs;
         if (mode == EMU_SPLIT_FP16) {
-            if (d_range_flag || range) EMU_RUN_TS(0, true);
-            else EMU_RUN_TS(0, false);
+            const int rmask = (d_range_flag ? 1 : 0) | (range ? 2 : 0);
+            if (rmask == 3) EMU_RUN_TS(0, 3);
+            else if (rmask == 2) EMU_RUN_TS(0, 2);
+            else if (rmask == 1) EMU_RUN_TS(0, 1);
+            else EMU_RUN_TS(0, 0);
         } else {
-            if (range) EMU_RUN_TS(1, true);
-            else EMU_RUN_TS(1, false);
+            if (range) EMU_RUN_TS(1, 2);
+            else EMU_RUN_TS(1, 0);
         }
         if (range && rs == EMU_STATUS_SUCCESS) g_last_launches = 2;   // max-|x| pass + GEMM
         return rs;

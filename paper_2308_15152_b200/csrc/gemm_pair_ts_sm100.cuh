@@ -110,10 +110,10 @@ __device__ __forceinline__ void ts_unit_tile(const GemmParams& p, long long u, i
 
 // TA / TB: op(A) = A^T (A stored k x m, k contiguous) / op(B) = B^T (B stored n x k):
 // only the TMA boxes and the splitters' shared-memory reads change (NEXT row 2)
-// RANGE: the FP16 overflow flag (p.range_flag) and the range-safe mode's power-of-two
-// scaling (p.row_max / p.col_max, R#22) are compiled in, each still enabled by its pointer.
+// RANGE (bit mask): 1 compiles in the FP16 overflow flag (p.range_flag), 2 the range-safe
+// mode's power-of-two scaling (p.row_max / p.col_max, R#22); each still enabled by its pointer.
 // MC: epilogue stores every tile to p.dst[0 .. num_dst-1] (fused all-gather, NEXT row 3)
-template <int MODE, bool RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false, bool MC = false>
+template <int MODE, int RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false, bool MC = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, SPLITC_, ASTAT_>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
@@ -408,13 +408,13 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t tq = tmem_base + ((q * 32u) << 16);
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0, unit_it = 0;
         uint32_t nonfinite = 0;
-        const bool chk = RANGE && p.range_flag != nullptr;   // the FP16 overflow flag was asked for
+        const bool chk = (RANGE & 1) && p.range_flag != nullptr;   // the FP16 overflow flag was asked for
         for (long long u = cid; u < num_units; u += ncl, ++unit_it) {
             for (int j = 0; j < R; ++j) {
                 const bool doA = !ASTAT || j == 0;
                 // range-safe mode: this thread's row of A and column of B scale by 2^-e
                 float sa = 1.0f, sb = 1.0f;
-                if (RANGE && p.row_max) {
+                if ((RANGE & 2) && p.row_max) {
                     int b, mt, nt;
                     ts_unit_tile<ASTAT>(p, u, j, b, mt, nt);
                     const int r = mt * 256 + (int)rank * Cfg::BM + (int)m;
@@ -470,7 +470,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         for (int c = 0; c < 2; ++c)
                             vb[c] = *reinterpret_cast<const float4*>(fb + n * 128 + (((2 * quarter + c) ^ (n & 7)) << 4));
                     }
-                    if (RANGE && p.row_max) {   // exact power-of-two scaling (RN where the result is subnormal)
+                    if ((RANGE & 2) && p.row_max) {   // exact power-of-two scaling (RN where the result is subnormal)
                         if (doA) {
 #pragma unroll
                             for (int jj = 0; jj < Cfg::KS; jj += 2) scale_f32x2(av[jj], av[jj + 1], sa);
@@ -547,7 +547,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 }
             }
         }
-        if (RANGE && p.range_flag) {
+        if ((RANGE & 1) && p.range_flag) {
             nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
             if (nonfinite && lane == 0) atomicOr(p.range_flag, 1u);
         }
@@ -685,7 +685,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 PROF_T0();
                 if (lane == 0) TRACE_AT(3 + e, 14, j);
                 const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
-                if (RANGE && p.row_max) {   // range-safe mode: C_acc * 2^f_j * 2^e_i (exact unless out of range)
+                if ((RANGE & 2) && p.row_max) {   // range-safe mode: C_acc * 2^f_j * 2^e_i (exact unless out of range)
                     const int r = mrow0 + (int)(q * 32 + lane);
                     const float ua = r < p.m ? pow2i(range_exp_of(p.row_max[(long long)b * p.m + r])) : 1.0f;
                     const int colb = nt * Cfg::BN + (int)(h * HALF);
