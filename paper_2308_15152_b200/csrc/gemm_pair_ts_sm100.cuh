@@ -17,8 +17,11 @@
 //             products (P2, P3 -> D_corr) and P1 (-> D_hi) of a k-block have their
 //             own full/empty barriers, so the drain of D_corr overlaps P1 and the
 //             drain of D_hi overlaps the next k-block's P2/P3;
+//   BN =  64: 2 buffers (256 columns) -- for problems with fewer 256 x 128 tiles
+//             than clusters (twice the clusters at work; c4);
 //   BN =  96: 2 buffers (384 columns) -- the MMA of k-block j+1 overlaps the
 //             drain of k-block j (kept for comparison, EMU_TS_N=96).
+// Streaming tiles load A with L2 evict_last and B with evict_first (p.l2_policy).
 // A-stationary (ASTAT, short k): the split A of a whole (batch item, 256-row block)
 // -- all k, hi and lo -- stays in TMEM (k <= 256 FP16, k <= 128 TF32) while the
 // cluster walks every n-tile of that row block, so A is loaded and split once per
