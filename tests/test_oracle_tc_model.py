@@ -75,7 +75,7 @@ def test_truncation_only_positive_terms(mode):
     loses < 2^-23 * S, so exact - model <= n_groups * ((G+1) 2^-F + 1) 2^-23 S."""
     rng = np.random.default_rng(11)
     K = 16 if mode == "fp16" else 8
-    G, F = oracle.TC_MODELS["sm100"]
+    G, F, _ = oracle.TC_MODELS["sm100"]
     for trial in range(200):
         k = int(rng.integers(1, 65))
         sig = rng.integers(1024, 2048, size=(2, k)).astype(np.float64)
@@ -97,7 +97,7 @@ def test_signed_terms_bound_and_odd_symmetry(mode):
     + 1) 2^-23 * (sum |products| + |partial sums|) <= 2 n_groups (...) sum|p|."""
     rng = np.random.default_rng(12)
     K = 16 if mode == "fp16" else 8
-    G, F = oracle.TC_MODELS["sm100"]
+    G, F, _ = oracle.TC_MODELS["sm100"]
     for trial in range(200):
         k = int(rng.integers(1, 65))
         sig = rng.integers(1024, 2048, size=(2, k)).astype(np.float64)
