@@ -101,6 +101,8 @@ def _args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", dest="secondary", action="store_false",
+                    help="skip the secondary records (c2 tf32, c3 fp16/tf32, c5) of the default run")
     return ap.parse_args()
 
 
@@ -346,31 +348,19 @@ def run_c3_sharded(args, rank, world, local):
     dist.destroy_process_group()
 
 
-def main():
-    args = _args()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+def measure(args, cfg_name, mode, rank, world, local, steps, warmup, e2e=True, cpu_baseline=True):
+    """Time `steps` emu_sgemm_batched calls of one workload on this rank (after
+    `warmup` untimed ones), max over ranks; accuracy, e2e, roofline, clocks.
+    Returns the JSON record (without the contract's top-level keys)."""
     import torch
     import torch.distributed as dist
 
     import paper_2308_15152_b200 as emu
-
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.config == "c3" and world > 1:
-        run_c3_sharded(args, rank, world, local)
-        return
-    cfg = workloads.CONFIGS[args.config]
+    cfg = workloads.CONFIGS[cfg_name]
     m, n, k = cfg.m, cfg.n, cfg.k
-    mode = args.mode
     # c5: a FIXED global batch split over the ranks (strong scaling, SURVEY §8(d));
     # every other batched config: its batch per rank (weak scaling, R#21)
-    strong = args.config == "c5"
+    strong = cfg_name == "c5"
     batch = cfg.batch // world if strong else cfg.batch
     item0 = rank * batch
 
@@ -382,7 +372,8 @@ def main():
     stream = torch.cuda.current_stream()
     sA, sB, sC = k * m, n * k, n * m
     # c4 in FP16 mode: the range-safe entry (R#22; plain FP16 overflows at 2^30)
-    use_range = args.config == "c4" and mode == "fp16"
+    use_range = cfg_name == "c4" and mode == "fp16"
+    ws = ws_bytes = None
     if use_range:
         ws_bytes = emu.emu_range_workspace_size(m, n, batch)
         ws = torch.empty(max(ws_bytes // 4, 4), dtype=torch.int32, device="cuda")
@@ -398,13 +389,13 @@ def main():
             emu.emu_sgemm_batched(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, stream)
         launches += emu.emu_last_launch_count()
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, warmup)):
         step()
     torch.cuda.synchronize()
     # c1 is launch-latency bound (16 x 64^3): each step is one replay of a CUDA graph
     # holding the launch, so the host launch path is not what is timed
     graph = None
-    if args.config == "c1":
+    if cfg_name == "c1":
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step()
@@ -418,7 +409,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             if graph is not None:
                 graph.replay()
                 launches += launches_per_step
@@ -430,8 +421,8 @@ def main():
         dist.barrier()
     ms_max = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     flops_step = 2.0 * m * n * k * batch * world
-    value = flops_step * args.steps / (ms_max / 1e3) / 1e12
-    ms_per_step = ms_max / args.steps
+    value = flops_step * steps / (ms_max / 1e3) / 1e12
+    ms_per_step = ms_max / steps
 
     # multi-GPU: every shard bit-identical to the single-GPU computation (outside timing)
     def recompute(g):
@@ -446,27 +437,26 @@ def main():
         return item_checksums(C1)[0]
     multi_check = cross_rank_check(item_checksums(dC), batch, recompute) if world > 1 else {}
 
-    # accuracy on sampled problems of this rank (outside the timed region)
+    # accuracy on sampled outputs of this rank (outside the timed region): relative
+    # Frobenius (north_star) and the paper's max relative error vs FP64,
+    # beside plain FP32 SGEMM (O5) on the same outputs
     import oracle
-    idx = [0, batch // 2, batch - 1] if batch > 1 else [0]
-    if batch > 1:
-        C_s = dC[idx].cpu().numpy()
-        R = oracle.gemm_f64(A_h[idx], B_h[idx], m, n, k)
-        S = oracle.sgemm_f32(A_h[idx], B_h[idx], m, n, k)
-        e_emu, e_sg = oracle.rel_frobenius(C_s, R), oracle.rel_frobenius(S, R)
-        acc_note = f"{len(idx)} problems"
-    else:
-        g = workloads.rng(5)
-        ii, jj = g.integers(0, m, 512), g.integers(0, n, 512)
-        got = dC[0][torch.from_numpy(jj), torch.from_numpy(ii)].cpu().numpy().astype(np.float64)
-        R = np.array([np.dot(A_h[0, :, i].astype(np.float64), B_h[0, j, :].astype(np.float64)) for i, j in zip(ii, jj)])
-        e_emu = float(np.linalg.norm(got - R) / np.linalg.norm(R))
-        e_sg = None
-        acc_note = "512 sampled outputs"
+    g = workloads.rng(5)
+    nsamp = 2048 if batch > 1 else 512
+    bb = g.integers(0, batch, nsamp)
+    ii, jj = g.integers(0, m, nsamp), g.integers(0, n, nsamp)
+    got = dC[torch.from_numpy(bb), torch.from_numpy(jj), torch.from_numpy(ii)].cpu().numpy()
+    R = oracle.gemm_f64_entries(A_h, B_h, m, n, k, bb, ii, jj)
+    S = oracle.sgemm_f32_entries(A_h, B_h, m, n, k, bb, ii, jj)
+    acc = {"rel_frobenius_vs_fp64": oracle.rel_frobenius(got, R),
+           "rel_frobenius_fp32_sgemm": oracle.rel_frobenius(S, R),
+           "max_rel_error_vs_fp64": oracle.max_rel_error(got, R),
+           "max_rel_error_fp32_sgemm": oracle.max_rel_error(S, R),
+           "accuracy_sample": f"{nsamp} sampled outputs (full k each) of this rank's C"}
 
     # e2e through the C ABI with pinned HOST buffers (H2D + compute + D2H per step)
-    e2e = None
-    if not args.no_e2e and not use_range:   # (the host entry has no range-safe form)
+    e2e_rec = None
+    if e2e and not use_range:   # (the host entry has no range-safe form)
         pA = torch.from_numpy(A_h).pin_memory()
         pB = torch.from_numpy(B_h).pin_memory()
         pC = torch.empty((batch, n, m)).pin_memory()
@@ -479,10 +469,11 @@ def main():
             emu.emu_sgemm_batched_host(m, n, k, 1.0, pA, m, sA, pB, k, sB, 0.0, pC, m, sC, batch, mode, stream)
         torch.cuda.synchronize()
         dt = max_over_ranks(time.perf_counter() - t0, device="cuda")
-        e2e = {"value": flops_step * args.e2e_steps / dt / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": int(pA.numel() * 4 + pB.numel() * 4),
-               "d2h_bytes_per_step": int(pC.numel() * 4), "steps": args.e2e_steps,
-               "api": "emu_sgemm_batched_host (pinned host buffers)"}
+        e2e_rec = {"value": flops_step * args.e2e_steps / dt / 1e12, "unit": UNIT,
+                   "h2d_bytes_per_step": int(pA.numel() * 4 + pB.numel() * 4),
+                   "d2h_bytes_per_step": int(pC.numel() * 4), "steps": args.e2e_steps,
+                   "api": "emu_sgemm_batched_host (pinned host buffers)"}
+        del pA, pB, pC
 
     peaks = _peaks()
     tc_peak = peaks["bf16_tflops"] * (1.0 if mode == "fp16" else 0.5)   # fp16 = bf16 rate; tf32 = 1/2 (nominal ratio)
@@ -490,49 +481,90 @@ def main():
     # cuBLAS measurement): its roofline uses the sustained peak; the burst fraction is
     # reported beside it
     tc_peak_sus = peaks["bf16_tflops_sustained"] * (1.0 if mode == "fp16" else 0.5)
-    kname = ("emu_sgemm_pair_ts_kernel<%s, 128 cols, split commit%s%s>"
-             % ("FP16" if mode == "fp16" else "TF32",
-                ", A-stationary" if (args.config in ("c2", "c5") and (mode == "fp16" or k <= 128)) else "",
-                ", range-safe (+ range_max_kernel)" if use_range else ""))
-    if args.config == "c1":
-        kname = "emu_sgemm_kernel<%s, 128 cols> (m <= 128: single-CTA tiles)" % ("FP16" if mode == "fp16" else "TF32")
-    if args.config in ("c1", "c2", "c5"):
+    kname = emu.emu_last_kernel_name()     # what the library dispatched for this workload
+    kernel_ms = ms_per_step / max(1, launches / steps)    # per launch of the dominant kernel
+    if cfg_name in ("c1", "c2", "c5"):
         bytes_launch = 4.0 * (m * k + k * n + m * n) * batch
-        achieved = bytes_launch / (ms_per_step / 1e3) / 1e9
+        achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(args.config, mode),
+                "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(cfg_name, mode),
                 "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peaks["source"],
                 "kernel": kname}
     else:
         tc_flops = 6.0 * m * n * k * batch
-        achieved = tc_flops / (ms_per_step / 1e3) / 1e12
+        achieved = tc_flops / (kernel_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tc_peak_sus, "unit": "TFLOP/s",
                 "frac": achieved / tc_peak_sus, "frac_of_burst_peak": achieved / tc_peak,
-                "burst_peak": tc_peak, "traffic": _traffic(args.config, mode),
+                "burst_peak": tc_peak, "traffic": _traffic(cfg_name, mode),
                 "algorithmic_flops_per_launch": tc_flops, "peak_source": peaks["source"] +
                 (" sustained bf16 peak (fp16 same rate)" if mode == "fp16"
                  else " sustained bf16 peak x 1/2 (nominal tf32 ratio)"),
                 "kernel": kname}
+        if use_range:
+            roof["note"] = "the range-safe call is two launches (max-|x| pass + GEMM); time per launch pair"
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if cpu_baseline and rank == 0 and world == 1:
         cpu = _cpu_baseline(cfg, mode, A_h, B_h)
 
     per_gpu = value / world
-    out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+    rec = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": max(3, warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": _config(cfg, mode, world, batch),
         "frac_fp32_simt_peak": per_gpu / FP32_SIMT_PEAK_TF,
         "frac_tc_peak_over_3": per_gpu / (tc_peak / 3.0),
         "frac_tc_sustained_peak_over_3": per_gpu / (tc_peak_sus / 3.0),
-        "rel_frobenius_vs_fp64": e_emu, "rel_frobenius_fp32_sgemm": e_sg, "accuracy_sample": acc_note,
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clk.summary(), "paper_context": PAPER_A100,
+        **acc,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e_rec, "gpu_launches": launches,
+        "clocks": clk.summary(),
     }
     if world > 1:
-        out["multi_gpu_check"] = multi_check
+        rec["multi_gpu_check"] = multi_check
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+    return rec
+
+
+# secondary records of the default run (each its own timing, clocks, roofline):
+# the large-shape target (c3, both splits), the TF32 split of the bench shape,
+# and c5's fixed global batch of 8192 (strong scaling over the ranks)
+SECONDARY_1GPU = [("c2", "tf32", 50), ("c3", "fp16", 10), ("c3", "tf32", 6), ("c5", "fp16", 30)]
+SECONDARY_NGPU = [("c5", "fp16", 30)]
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == "c3" and world > 1:
+        run_c3_sharded(args, rank, world, local)
+        return
+    out = measure(args, args.config, args.mode, rank, world, local, args.steps, args.warmup,
+                  e2e=not args.no_e2e, cpu_baseline=not args.no_cpu_baseline)
+    out["paper_context"] = PAPER_A100
+    if args.secondary and args.config == "c2" and args.mode == "fp16":
+        sec = []
+        for cname, cmode, csteps in (SECONDARY_1GPU if world == 1 else SECONDARY_NGPU):
+            r = measure(args, cname, cmode, rank, world, local, csteps, 3, e2e=False, cpu_baseline=False)
+            sec.append({key: r[key] for key in ("value", "unit", "ms_per_step", "steps", "scaling", "config",
+                                                "frac_fp32_simt_peak", "frac_tc_peak_over_3",
+                                                "frac_tc_sustained_peak_over_3", "rel_frobenius_vs_fp64",
+                                                "rel_frobenius_fp32_sgemm", "max_rel_error_vs_fp64",
+                                                "max_rel_error_fp32_sgemm", "accuracy_sample", "roofline",
+                                                "gpu_launches", "clocks") + (("multi_gpu_check",) if world > 1 else ())})
+        out["secondary"] = sec
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

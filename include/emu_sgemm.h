@@ -158,7 +158,7 @@ emu_status emu_sgemm_batched_layout(emu_layout layout, char transa, char transb,
  *   (0 when the row / column has no finite non-zero element),
  * so every scaled row / column peaks in [2^14, 2^15); runs the unchanged
  * method (split, three products, per-k-block combine) on the scaled operands;
- * and un-scales the combined accumulator: C = RN(alpha*((C'*2^f_j)*2^e_i) +
+ * and un-scales the combined accumulator: C = RN(alpha*RN(C'*2^(e_i+f_j)) +
  * RN(beta*C)).  Power-of-two scaling is exact except where a scaled value is
  * subnormal or overflows.  The exponents come from one max-|x| pass over A
  * and B (a second kernel, recorded by emu_last_launch_count).
@@ -279,6 +279,12 @@ emu_status emu_tcec_scan(int n, int count, const float* X, int ldx, float* Y, in
 /* Number of kernel launches the last successful call on this host thread
  * issued (0 for a quick return without a scale kernel); for launch accounting. */
 int emu_last_launch_count(void);
+
+/* Name of the GEMM kernel (and its template configuration) the last call on
+ * this host thread dispatched; "" before any launch.  Never NULL; the string
+ * is owned by the library and stays valid.  For reports (bench.py) and
+ * diagnostics; the dispatch itself is described in DESIGN.md §6. */
+const char* emu_last_kernel_name(void);
 
 /* Human-readable status. Never NULL. */
 const char* emu_status_string(emu_status status);

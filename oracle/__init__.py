@@ -90,6 +90,10 @@ def lib():
         L.orc_sgemm_f32_batched.restype = None
         L.orc_tc_chain.argtypes = [i32, i32, i32, i32, i32, i32, i32, P, P, P, P]
         L.orc_tc_chain.restype = i32
+        L.orc_gemm_f64_entries.argtypes = [i32, P, i64, i64, P, i64, i64, i64, P, P, P, P]
+        L.orc_gemm_f64_entries.restype = None
+        L.orc_sgemm_f32_entries.argtypes = [i32, P, i64, i64, P, i64, i64, i64, P, P, P, P]
+        L.orc_sgemm_f32_entries.restype = None
         L.orc_max_threads.argtypes = []; L.orc_max_threads.restype = i32
         L.orc_set_threads.argtypes = [i32]; L.orc_set_threads.restype = None
         _lib = L
@@ -371,6 +375,28 @@ def sgemm_f32(A, B, m, n, k, alpha=1.0, beta=0.0, C=None, ldc=None):
     lib().orc_sgemm_f32_batched(m, n, k, alpha, _p(A), lda, sA, _p(B), ldb, sB,
                                 beta, _p(C), ldc, n * ldc, batch)
     return C
+
+
+def _entries_args(A, B, m, n, k, bidx, ii, jj):
+    A, B, batch, lda, ldb, sA, sB = _batched_args(A, B, m, n, k)
+    idx = [np.ascontiguousarray(v, dtype=np.int64) for v in (bidx, ii, jj)]
+    return A, B, lda, ldb, sA, sB, idx
+
+
+def gemm_f64_entries(A, B, m, n, k, bidx, ii, jj):
+    """O4 (binary64, ascending p) at entries C_{bidx}(ii, jj); alpha = 1, beta = 0"""
+    A, B, lda, ldb, sA, sB, idx = _entries_args(A, B, m, n, k, bidx, ii, jj)
+    out = np.empty(len(idx[0]), dtype=np.float64)
+    lib().orc_gemm_f64_entries(k, _p(A), lda, sA, _p(B), ldb, sB, len(out), *map(_p, idx), _p(out))
+    return out
+
+
+def sgemm_f32_entries(A, B, m, n, k, bidx, ii, jj):
+    """O5 (sequential binary32 FMA) at entries C_{bidx}(ii, jj); alpha = 1, beta = 0"""
+    A, B, lda, ldb, sA, sB, idx = _entries_args(A, B, m, n, k, bidx, ii, jj)
+    out = np.empty(len(idx[0]), dtype=np.float32)
+    lib().orc_sgemm_f32_entries(k, _p(A), lda, sA, _p(B), ldb, sB, len(out), *map(_p, idx), _p(out))
+    return out
 
 
 # -------------------------------------------------------------- metrics ----

@@ -604,7 +604,7 @@ int orc_emu_gemm_entries(int mode, int corr_enable, int m, int n, int k, int kb,
 /* so the largest scaled magnitude lies in [2^14, 2^15); then runs the       */
 /* unchanged emulation (Eqs. corr-1..5 with the per-k-block combine) on      */
 /* A' = A 2^-e, B' = B 2^-f, and undoes the scaling on C_reg:                */
-/*   C(i,j) = RN(alpha * ((C'(i,j) * 2^f_j) * 2^e_i) + RN(beta * C0(i,j))).   */
+/*   C(i,j) = RN(alpha * RN(C'(i,j) * 2^(e_i + f_j)) + RN(beta * C0(i,j))).   */
 /* Each scaling is one correctly rounded ldexpf (exact unless the result is  */
 /* subnormal or overflows).                                                  */
 /* ------------------------------------------------------------------------ */
@@ -628,9 +628,12 @@ void orc_range_exponents(int m, int n, int k, const float* A, int64_t lda,
     for (int j = 0; j < n; ++j) f_cols[j] = range_exp(B + (int64_t)j * ldb, k, 1);
 }
 
+/* C = RN(alpha * RN(C' * 2^(e+f)) + bc): the unscaling is ONE correctly     */
+/* rounded scaling by the combined exponent (R#22), so a tiny row times a    */
+/* huge column cannot overflow or underflow in an intermediate step           */
 static float range_unscale(float alpha, float c_reg, int f, int e, float bc)
 {
-    return fmaf(alpha, ldexpf(ldexpf(c_reg, f), e), bc);
+    return fmaf(alpha, ldexpf(c_reg, e + f), bc);
 }
 
 int orc_emu_gemm_range_batched(int mode, int corr_enable, int m, int n, int k, int kb,
@@ -782,6 +785,39 @@ void orc_sgemm_f32_batched(int m, int n, int k, float alpha,
                 float bc = (beta != 0.0f) ? beta * Cb[i + (int64_t)j * ldc] : 0.0f;
                 Cb[i + (int64_t)j * ldc] = fmaf(alpha, acc, bc);
             }
+    }
+}
+
+/* O4 and O5 at selected entries C_{bidx[e]}(ii[e], jj[e]) (alpha = 1,      */
+/* beta = 0): the same loops as above, for sampled accuracy gates at sizes    */
+/* the full reference cannot reach (c3).                                     */
+void orc_gemm_f64_entries(int k, const float* A, int64_t lda, int64_t strideA,
+                          const float* B, int64_t ldb, int64_t strideB, int64_t nent,
+                          const int64_t* bidx, const int64_t* ii, const int64_t* jj, double* out)
+{
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < nent; ++e) {
+        const float* Ab = A + bidx[e] * strideA;
+        const float* Bb = B + bidx[e] * strideB;
+        double acc = 0.0;
+        for (int p = 0; p < k; ++p)
+            acc += (double)Ab[ii[e] + (int64_t)p * lda] * (double)Bb[p + jj[e] * ldb];
+        out[e] = acc;
+    }
+}
+
+void orc_sgemm_f32_entries(int k, const float* A, int64_t lda, int64_t strideA,
+                           const float* B, int64_t ldb, int64_t strideB, int64_t nent,
+                           const int64_t* bidx, const int64_t* ii, const int64_t* jj, float* out)
+{
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < nent; ++e) {
+        const float* Ab = A + bidx[e] * strideA;
+        const float* Bb = B + bidx[e] * strideB;
+        float acc = 0.0f;
+        for (int p = 0; p < k; ++p)
+            acc = fmaf(Ab[ii[e] + (int64_t)p * lda], Bb[p + jj[e] * ldb], acc);
+        out[e] = acc;
     }
 }
 

@@ -15,7 +15,7 @@ import os
 __all__ = [
     "EMU_SPLIT_FP16", "EMU_SPLIT_TF32", "EMU_FLAG_NO_CORRECTION", "EmuError", "lib", "LIB_PATH",
     "emu_sgemm", "emu_sgemm_batched", "emu_sgemm_batched_ex", "emu_sgemm_batched_host",
-    "emu_split", "emu_status_string", "emu_version", "emu_last_launch_count", "mode_of",
+    "emu_split", "emu_status_string", "emu_version", "emu_last_launch_count", "emu_last_kernel_name", "mode_of",
     "EMU_FLAG_SIMT", "emu_tcec_gemm_batched", "emu_tcec_householder_batched", "emu_tcec_givens_batched",
     "emu_tcec_scan", "emu_sgemm_multicast", "EMU_COL_MAJOR", "EMU_ROW_MAJOR", "emu_sgemm_batched_layout",
     "matmul",
@@ -85,6 +85,8 @@ lib.emu_version.argtypes = []
 lib.emu_version.restype = _i
 lib.emu_last_launch_count.argtypes = []
 lib.emu_last_launch_count.restype = _i
+lib.emu_last_kernel_name.argtypes = []
+lib.emu_last_kernel_name.restype = ctypes.c_char_p
 
 
 def mode_of(mode) -> int:
@@ -272,3 +274,7 @@ def emu_version() -> int:
 
 def emu_last_launch_count() -> int:
     return lib.emu_last_launch_count()
+
+
+def emu_last_kernel_name() -> str:
+    return lib.emu_last_kernel_name().decode()

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -21,6 +22,18 @@
 namespace {
 
 thread_local int g_last_launches = 0;
+// name of the GEMM kernel the last call on this host thread dispatched (diagnostics)
+thread_local const char* g_last_kernel = "";
+
+// one static name per kernel instantiation, built once
+template <typename F>
+const char* kernel_name_once(F build)
+{
+    static char buf[192];
+    static std::once_flag once;
+    std::call_once(once, [&] { build(buf, sizeof(buf)); });
+    return buf;
+}
 
 // extra result destinations of the emu_sgemm_multicast call in progress on this
 // host thread (nullptr otherwise); read by the TS-kernel launcher
@@ -290,6 +303,10 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     const long long grid = std::min<long long>(p.num_tiles, sms);
     emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE, LDG><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     g_last_launches = 1;
+    g_last_kernel = kernel_name_once([](char* b, size_t nb) {
+        snprintf(b, nb, "emu_sgemm_kernel<%s, BN=%d, A layout %d%s%s> (single CTA, M=128)", MODE == 0 ? "FP16" : "TF32",
+                 BN, ALAY, RANGE ? ", range flag" : "", LDG ? ", direct loads" : "");
+    });
     return launch_status(cudaGetLastError());
 }
 
@@ -358,6 +375,10 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     emu::emu_sgemm_pair_kernel<MODE, ALAY, RANGE>
         <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     g_last_launches = 1;
+    g_last_kernel = kernel_name_once([](char* b, size_t nb) {
+        snprintf(b, nb, "emu_sgemm_pair_kernel<%s, A layout %d%s> (CTA pair, both operands in SMEM)",
+                 MODE == 0 ? "FP16" : "TF32", ALAY, RANGE ? ", range flag" : "");
+    });
     return launch_status(cudaGetLastError());
 }
 
@@ -466,6 +487,13 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
             <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
     }
     g_last_launches = 1;
+    g_last_kernel = kernel_name_once([](char* b, size_t nb) {
+        snprintf(b, nb, "emu_sgemm_pair_ts_kernel<%s, %d cols%s%s%s%s%s%s> (CTA pair, A in TMEM)",
+                 MODE == 0 ? "FP16" : "TF32", BN, SPLITC ? ", split commit" : "", ASTAT ? ", A-stationary" : "",
+                 (RANGE & 2) ? ", range-safe" : "", (RANGE & 1) ? ", range flag" : "", TA ? ", op(A)=T" : "",
+                 TB ? ", op(B)=T" : "");
+    });
+    if (launched) g_last_kernel = "emu_sgemm_pair_ts_kernel<multicast epilogue> (CTA pair, A in TMEM)";
     return launch_status(cudaGetLastError());
 }
 
@@ -489,6 +517,8 @@ __attribute__((visibility("default"))) const char* emu_status_string(emu_status 
 __attribute__((visibility("default"))) int emu_version(void) { return EMU_VERSION; }
 
 __attribute__((visibility("default"))) int emu_last_launch_count(void) { return g_last_launches; }
+
+__attribute__((visibility("default"))) const char* emu_last_kernel_name(void) { return g_last_kernel; }
 
 // default combine interval KB (R#7): 64 up to k = 8192, doubled for every further
 // factor 4 of k (128 up to 32768, ...).  With the measured tensor-core model the
@@ -589,7 +619,7 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     // with more than one 128-row block; the SMEM-operand pair kernel stays selectable
     // (EMU_KERNEL=pair) for comparison.
     if ((ta || tb) && !tma_ok) return EMU_STATUS_NOT_SUPPORTED;   // transposed operands: TS kernel only
-    if (g_mdst && !tma_ok) return EMU_STATUS_NOT_SUPPORTED;   // multicast: TS kernel only
+    if (g_mdst && (!tma_ok || ldg)) return EMU_STATUS_NOT_SUPPORTED;   // multicast: TS kernel only (also under EMU_FORCE_LDG)
     const bool ts = !ldg && (range || ta || tb || g_mdst || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     const bool pair = !ldg && !ts && (kernel_pref == 2 || kernel_pref == 3 || (kernel_pref == 0 && m > 128));
     // tile width of the TS kernel (profiles/r01_summary.md): 128 with one accumulator

@@ -688,15 +688,14 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 PROF_T0();
                 if (lane == 0) TRACE_AT(3 + e, 14, j);
                 const int mrow0 = mt * 256 + (int)rank * Cfg::BM;
-                if ((RANGE & 2) && p.row_max) {   // range-safe mode: C_acc * 2^f_j * 2^e_i (exact unless out of range)
+                if ((RANGE & 2) && p.row_max) {   // range-safe mode: C_acc * 2^(e_i + f_j), one rounding (R#22)
                     const int r = mrow0 + (int)(q * 32 + lane);
-                    const float ua = r < p.m ? pow2i(range_exp_of(p.row_max[(long long)b * p.m + r])) : 1.0f;
+                    const int er = r < p.m ? range_exp_of(p.row_max[(long long)b * p.m + r]) : 0;
                     const int colb = nt * Cfg::BN + (int)(h * HALF);
 #pragma unroll
                     for (int jj = 0; jj < HALF; ++jj) {
-                        const float ub = colb + jj < p.n
-                                             ? pow2i(range_exp_of(p.col_max[(long long)b * p.n + colb + jj])) : 1.0f;
-                        creg[jj] = __fmul_rn(__fmul_rn(creg[jj], ub), ua);
+                        const int fc = colb + jj < p.n ? range_exp_of(p.col_max[(long long)b * p.n + colb + jj]) : 0;
+                        creg[jj] = ldexp_rn(creg[jj], er + fc);
                     }
                 }
                 if (p.tma_store) {

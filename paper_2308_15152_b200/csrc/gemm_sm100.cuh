@@ -138,6 +138,17 @@ __device__ __forceinline__ int range_exp_of(unsigned int maxbits)
 }
 __device__ __forceinline__ float pow2i(int t) { return __int_as_float((127 + t) << 23); }
 
+// c * 2^t correctly rounded (one rounding, like ldexpf) for |t| <= 252: two
+// power-of-two factors of which only the second can round -- for t > 127 the
+// first (2^127) is exact unless it overflows (then so does the result); for
+// t < -126 the first (2^(t+126)) is exact unless the result is below 2^-252,
+// where both the two-step product and the exact result round to zero
+__device__ __forceinline__ float ldexp_rn(float c, int t)
+{
+    const int t2 = t > 127 ? t - 127 : (t < -126 ? -126 : 0);
+    return __fmul_rn(__fmul_rn(c, pow2i(t - t2)), pow2i(t2));
+}
+
 // A operand layouts in the operand ring
 enum : int {
     A_MN_SW128 = 0,      // MN-major, SWIZZLE_128B (16-bit elements; FP16 mode)

@@ -3,8 +3,11 @@ NEXT 3): B and C are split into contiguous column blocks, A is replicated, and
 each rank computes its block C[:, n0:n1] = A B[:, n0:n1] with
 emu_sgemm_multicast, whose epilogue stores every finished tile into EVERY
 rank's C buffer (symmetric-memory peer pointers over NVLink) -- the all-gather
-is fused into the GEMM and overlaps the remaining tiles.  A device-side
-barrier across the ranks then makes every C complete.
+is fused into the GEMM and overlaps the remaining tiles.  Two device-side
+barriers across the ranks, both on the stream the GEMM runs on, order each
+step: one BEFORE the first remote store (no rank may overwrite a peer's C
+while that peer still reads the previous step's result -- write-after-read),
+one after the last (every C is complete when the call's work is done).
 
 Host logic only (argument marshalling and the shard plan); the arithmetic runs
 in libemusgemm.so.  Without symmetric memory (a single process, or a backend
@@ -64,14 +67,22 @@ class ShardedGemm:
                              else "baseline: local block, then torch.distributed all_gather")
 
     def __call__(self, A, B_r, mode="fp16", stream=None, kblock=0, flags=0) -> None:
+        """One step, enqueued on `stream` (a torch.cuda.Stream; default: the
+        current stream).  The caller may read C after the step's work on that
+        stream; a later step first waits (device barrier) until every rank has
+        reached it, i.e. finished whatever it enqueued before on its stream."""
         m, k = self.m, self.k
         n0, n1 = self.n0, self.n1
         if self._ptrs is not None:
+            import torch
             import paper_2308_15152_b200 as emu
             dsts = [p + 4 * n0 * m for p in self._ptrs]
-            if n1 > n0:
-                emu.emu_sgemm_multicast(m, n1 - n0, k, 1.0, A, m, B_r, k, dsts, m, mode, stream, kblock, flags)
-            self._hdl.barrier()
+            st = stream if stream is not None else torch.cuda.current_stream()
+            with torch.cuda.stream(st):
+                self._hdl.barrier(channel=0)     # peers are done with their previous C (WAR)
+                if n1 > n0:
+                    emu.emu_sgemm_multicast(m, n1 - n0, k, 1.0, A, m, B_r, k, dsts, m, mode, st, kblock, flags)
+                self._hdl.barrier(channel=1)     # every block has landed in every C
             return
         self._compute_local(A, B_r, self.C[n0:n1], mode, stream, kblock, flags)
         if self.world > 1:

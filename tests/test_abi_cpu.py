@@ -82,6 +82,7 @@ def test_invalid_arguments_rejected_before_launch(emu, kw):
 def test_quick_return_without_device(emu, kw):
     assert _call(emu, **kw) == 0
     assert emu.emu_last_launch_count() == 0
+    assert isinstance(emu.emu_last_kernel_name(), str)
 
 
 def test_ex_validation(emu):

@@ -16,7 +16,7 @@ import pytest
 
 import oracle
 import workloads
-from gpu_util import assert_bits_equal, emu_gpu, emu_gpu_range
+from gpu_util import assert_bits_equal, emu_gpu, emu_gpu_range, tolerance
 
 pytestmark = pytest.mark.gpu
 MODES = ["fp16", "tf32"]
@@ -121,6 +121,12 @@ def test_default_kblock_rule(mode):
     C = emu_gpu(mode, A, B, m, n, k)
     assert np.array_equal(C, emu_gpu(mode, A, B, m, n, k, kblock=128))
     assert_bits_equal(C, oracle.emu_gemm(mode, A, B, m, n, k, tc="sm100"))
+    # model-free bars at this k: the element-wise bound against the ideal model
+    # and north_star's accuracy gate (rel-Frobenius <= 2x plain FP32 SGEMM)
+    d = np.abs(C.astype(np.float64) - oracle.emu_gemm(mode, A, B, m, n, k))
+    assert np.all(d <= tolerance(mode, A, B, m, n, k))
+    R = oracle.gemm_f64(A, B, m, n, k)
+    assert oracle.rel_frobenius(C, R) <= 2 * oracle.rel_frobenius(oracle.sgemm_f32(A, B, m, n, k), R)
 
 
 @pytest.mark.parametrize("mode", MODES)

@@ -13,7 +13,7 @@ import pytest
 import oracle
 import workloads
 from oracle import structured
-from gpu_util import assert_bits_equal, tolerance
+from gpu_util import assert_bits_equal, tolerance, tolerance_abab
 
 pytestmark = pytest.mark.gpu
 MODES = ["fp16", "tf32"]
@@ -44,8 +44,8 @@ def _tcec_gemm(mode, A, B, m, n, k, flags=0, alpha=1.0, beta=0.0, C=None, kblock
 def _simt_tol(mode, A, B, m, n, k, kb=64):
     """SIMT backend: sequential FP32 FMA over each k-block (KB - 1 roundings of
     the running block sum, u each) instead of the tensor core's per-instruction
-    truncation; the rest as tolerance()."""
-    t = tolerance(mode, A, B, m, n, k) / (2 * (kb / (16 if mode == "fp16" else 8)) + 4 + 2 * math.ceil(k / kb))
+    truncation; the rest as tolerance_abab()."""
+    t = tolerance_abab(mode, A, B, m, n, k) / (2 * (kb / (16 if mode == "fp16" else 8)) + 4 + 2 * math.ceil(k / kb))
     return (kb + 4 + 2 * math.ceil(k / kb)) * t
 
 
@@ -58,7 +58,8 @@ def test_tcec_gemm_parity(mode, flags):
     A, B = workloads.make_operands(batch, m, n, k, seed=61)
     C = _tcec_gemm(mode, A, B, m, n, k, flags=flags)
     ref = oracle.emu_gemm(mode, A, B, m, n, k, corr=not (flags & NO_CORR))
-    tol = (_simt_tol if flags & SIMT else tolerance)(mode, A, B, m, n, k)
+    tol = _simt_tol(mode, A, B, m, n, k) if flags & SIMT else \
+        tolerance(mode, A, B, m, n, k, 64, corr=not (flags & NO_CORR))
     err = np.abs(C.astype(np.float64) - ref)
     assert np.all(err <= tol), np.max(err / tol)
     # bit for bit with the oracle's model of the backend (R#9 / R#26)
@@ -93,7 +94,7 @@ def test_tcec_gemm_alpha_beta_and_kblock(mode):
     for kb in (0, 128):
         C = _tcec_gemm(mode, A, B, m, n, k, alpha=0.5, beta=-1.5, C=C0, kblock=kb)
         ref = oracle.emu_gemm(mode, A, B, m, n, k, alpha=0.5, beta=-1.5, C=C0, kb=kb or 64)
-        tol = 0.5 * tolerance(mode, A, B, m, n, k, kblock=kb or 64) + 2 * U * np.abs(ref)
+        tol = 0.5 * tolerance_abab(mode, A, B, m, n, k, kblock=kb or 64) + 2 * U * np.abs(ref)
         assert np.all(np.abs(C.astype(np.float64) - ref) <= tol)
         assert_bits_equal(C, oracle.emu_gemm(mode, A, B, m, n, k, alpha=0.5, beta=-1.5, C=C0, kb=kb or 64,
                                              tc="sm100"))
@@ -141,7 +142,7 @@ def test_householder_generated_operand(mode, m):
     for b in range(batch):
         Hc = workloads.colmajor(structured.householder_matrix(V[b]))[None]
         ref = oracle.emu_gemm(mode, Hc, X[b:b + 1], m, n, m)
-        tol = tolerance(mode, Hc, X[b:b + 1], m, n, m)
+        tol = tolerance_abab(mode, Hc, X[b:b + 1], m, n, m)
         assert np.all(np.abs(C[b:b + 1].astype(np.float64) - ref) <= tol), b
         assert_bits_equal(C[b:b + 1], oracle.emu_gemm(mode, Hc, X[b:b + 1], m, n, m, tc="sm100"))
 
@@ -173,7 +174,7 @@ def test_givens_map_operand(mode, mij):
     for b in range(batch):
         Gc = workloads.colmajor(structured.givens_matrix(m, i, j, *CS[b]))[None]
         ref = oracle.emu_gemm(mode, Gc, X[b:b + 1], m, n, m)
-        assert np.all(np.abs(C[b:b + 1].astype(np.float64) - ref) <= tolerance(mode, Gc, X[b:b + 1], m, n, m))
+        assert np.all(np.abs(C[b:b + 1].astype(np.float64) - ref) <= tolerance_abab(mode, Gc, X[b:b + 1], m, n, m))
         assert_bits_equal(C[b:b + 1], oracle.emu_gemm(mode, Gc, X[b:b + 1], m, n, m, tc="sm100"))
 
 
@@ -196,7 +197,7 @@ def test_scan_generated_operand(mode, n):
     Y = _scan(mode, n, count, X)
     Lc = workloads.colmajor(structured.scan_matrix(n))[None]
     ref = oracle.emu_gemm(mode, Lc, X[None], n, count, n)[0]
-    assert np.all(np.abs(Y.astype(np.float64) - ref) <= tolerance(mode, Lc, X[None], n, count, n)[0])
+    assert np.all(np.abs(Y.astype(np.float64) - ref) <= tolerance_abab(mode, Lc, X[None], n, count, n)[0])
     assert_bits_equal(Y, oracle.emu_gemm(mode, Lc, X[None], n, count, n, tc="sm100")[0])
 
 

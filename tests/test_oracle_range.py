@@ -128,3 +128,27 @@ def test_range_entries_match_full():
     b, i, j = g.integers(0, 3, 64), g.integers(0, m, 64), g.integers(0, n, 64)
     got = oracle.emu_gemm_range_entries("fp16", A, B, m, n, k, b, i, j, alpha=0.5, beta=2.0, C=C0)
     assert np.array_equal(got, full[b, j, i])
+
+
+def _tiny_rows_huge_cols(k=1024, m=24, n=20, seed=77):
+    """rows of A near 2^-100 and columns of B near 2^120 (some rows / columns
+    at ordinary magnitudes): the entries of A B lie near 2^20, well inside
+    binary32, but (C' * 2^f) alone would overflow -- the case the combined
+    exponent of R#22 exists for (round-2 advisor finding)"""
+    g = workloads.rng(seed)
+    A = g.uniform(-1, 1, size=(1, k, m)).astype(np.float32)
+    B = g.uniform(-1, 1, size=(1, n, k)).astype(np.float32)
+    A[:, :, : m - 4] *= np.float32(2.0 ** -100)
+    B[:, : n - 3, :] *= np.float32(2.0 ** 120)
+    return A, B, m, n, k
+
+
+@pytest.mark.parametrize("mode", ["fp16", "tf32"])
+def test_range_tiny_rows_times_huge_columns(mode):
+    A, B, m, n, k = _tiny_rows_huge_cols()
+    e, f = oracle.range_exponents(A[0], B[0], m, n, k)
+    assert e.min() <= -113 and f.max() >= 105           # the scaling really is extreme
+    C = oracle.emu_gemm_range(mode, A, B, m, n, k)
+    assert np.all(np.isfinite(C))
+    R = oracle.gemm_f64(A, B, m, n, k)
+    assert oracle.rel_frobenius(C, R) <= 2 * oracle.rel_frobenius(oracle.sgemm_f32(A, B, m, n, k), R)

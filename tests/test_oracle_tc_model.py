@@ -114,21 +114,27 @@ def test_signed_terms_bound_and_odd_symmetry(mode):
 
 
 @pytest.mark.parametrize("mode", ["fp16", "tf32"])
-def test_general_inputs_within_gpu_tolerance(mode):
-    """The sm100 model and the ideal model both stay within the element-wise
-    bound the parity tests use of the exact emulated product."""
+@pytest.mark.parametrize("k", [200, 4096, 16384])
+def test_general_inputs_within_gpu_tolerance(mode, k):
+    """The sm100 model stays within the element-wise bar the GPU parity tests
+    use against the ideal model (tests/gpu_util.py entry_bound),
+    and the bar discriminates: dropping the correction products, or doubling
+    their 2^-11 scale (C_on + (C_on - C_off)), exceeds it at every k."""
+    from gpu_util import tolerance_entries
     rng = np.random.default_rng(13)
-    m, n, k = 12, 10, 200
-    A = rng.uniform(-1, 1, size=(k, m)).astype(np.float32)
-    B = rng.uniform(-1, 1, size=(n, k)).astype(np.float32)
-    Cs = oracle.emu_gemm(mode, A, B, m, n, k, tc="sm100")[0].astype(np.float64)
-    R = oracle.gemm_f64(A, B, m, n, k)[0]
-    absAB = oracle.absgemm_f64(A, B, m, n, k)
-    kinst = 16 if mode == "fp16" else 8
-    gamma = 2 * (64 / kinst) + 4 + 2 * math.ceil(k / 64) + 8    # + split error of the operands
-    assert np.all(np.abs(Cs - R) <= gamma * 2.0 ** -24 * absAB)
-    Ci = oracle.emu_gemm(mode, A, B, m, n, k, tc="ideal")[0].astype(np.float64)
-    assert np.any(Cs != Ci)          # the two models really differ on general inputs
+    m = n = 24
+    A = rng.uniform(-1, 1, size=(1, k, m)).astype(np.float32)
+    B = rng.uniform(-1, 1, size=(1, n, k)).astype(np.float32)
+    b = np.zeros(32, dtype=np.int64)
+    i, j = rng.integers(0, m, 32), rng.integers(0, n, 32)
+    ideal = oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="ideal").astype(np.float64)
+    hw = oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="sm100").astype(np.float64)
+    off = oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="sm100", corr=False).astype(np.float64)
+    tol = tolerance_entries(mode, A, B, k, b, i, j)
+    assert np.all(np.abs(hw - ideal) <= tol)
+    assert np.any(hw != ideal)          # the two models really differ on general inputs
+    assert np.mean(np.abs(off - ideal) > tol) > 0.5
+    assert np.mean(np.abs(2 * hw - off - ideal) > tol) > 0.5
 
 
 @pytest.mark.parametrize("mode", ["fp16", "tf32"])
