@@ -185,38 +185,50 @@ def _traffic(config, mode):
     return v.get("dram_bytes_per_launch") if isinstance(v, dict) else None
 
 
-def _cpu_baseline(cfg, mode, A_host, B_host, budget_s=15.0):
+def _cpu_baseline(cfg, mode, A_host, B_host, budget_s=15.0, budget_1core_s=5.0):
     """The oracle as it stands (emulation model O3), on this host's cores, on a
-    bounded sample of the same workload."""
+    bounded sample of the same workload; and the same on ONE core (a smaller
+    sample), so the core count behind the number is explicit."""
     import oracle
     m, n, k = cfg.m, cfg.n, cfg.k
     cores = oracle.max_threads()
-    if cfg.batch > 1:
-        t0 = time.perf_counter()
-        oracle.emu_gemm(mode, A_host[:1], B_host[:1], m, n, k)
-        t1 = time.perf_counter() - t0
-        cnt = int(max(1, min(cfg.batch, budget_s / max(t1, 1e-6))))
-        t0 = time.perf_counter()
-        oracle.emu_gemm(mode, A_host[:cnt], B_host[:cnt], m, n, k)
-        dt = time.perf_counter() - t0
-        flops = 2.0 * m * n * k * cnt
-        sample = f"{cnt} of {cfg.batch} problems ({m}x{n}x{k}), full oracle emulation model"
-    else:
+
+    def timed(budget):
+        if cfg.batch > 1:
+            t0 = time.perf_counter()
+            oracle.emu_gemm(mode, A_host[:1], B_host[:1], m, n, k)
+            t1 = time.perf_counter() - t0
+            cnt = int(max(1, min(cfg.batch, budget / max(t1, 1e-6))))
+            t0 = time.perf_counter()
+            oracle.emu_gemm(mode, A_host[:cnt], B_host[:cnt], m, n, k)
+            dt = time.perf_counter() - t0
+            return 2.0 * m * n * k * cnt, dt, f"{cnt} of {cfg.batch} problems ({m}x{n}x{k}), full oracle emulation model"
         # sampled entries of the single large GEMM
-        nent = 4096
-        g = workloads.rng(99)
-        ii = g.integers(0, m, nent)
-        jj = g.integers(0, n, nent)
-        bb = np.zeros(nent, dtype=np.int64)
-        t0 = time.perf_counter()
         entries = oracle.emu_gemm_range_entries if (cfg.dist == "logu30" and mode == "fp16") \
             else oracle.emu_gemm_entries
-        entries(mode, A_host, B_host, m, n, k, bb, ii, jj)
-        dt = time.perf_counter() - t0
-        flops = 2.0 * k * nent
-        sample = f"{nent} sampled outputs of the {m}x{n}x{k} GEMM (full k each)"
-    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": sample, "seconds": round(dt, 3)}
+        g = workloads.rng(99)
+        nent = 64
+        ii, jj = g.integers(0, m, 1 << 16), g.integers(0, n, 1 << 16)
+        while True:
+            bb = np.zeros(nent, dtype=np.int64)
+            t0 = time.perf_counter()
+            entries(mode, A_host, B_host, m, n, k, bb, ii[:nent], jj[:nent])
+            dt = time.perf_counter() - t0
+            if dt > 0.25 * budget or nent >= (1 << 16):
+                break
+            nent = min(1 << 16, nent * max(2, int(0.5 * budget / max(dt, 1e-6))))
+        return 2.0 * k * nent, dt, f"{nent} sampled outputs of the {m}x{n}x{k} GEMM (full k each)"
+
+    flops, dt, sample = timed(budget_s)
+    rec = {"value": flops / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": sample, "seconds": round(dt, 3)}
+    oracle.set_threads(1)
+    try:
+        f1, d1, s1 = timed(budget_1core_s)
+    finally:
+        oracle.set_threads(cores)
+    rec["one_core"] = {"value": f1 / d1 / 1e12, "unit": UNIT, "cores": 1, "sample": s1, "seconds": round(d1, 3)}
+    return rec
 
 
 def run_reference(args):

@@ -226,6 +226,28 @@ int env_int(const char* name, int dflt, int lo, int hi)
     return e ? std::max(lo, std::min(hi, atoi(e))) : dflt;
 }
 
+// Launch with programmatic stream serialization (PDL): the GEMM kernels call
+// griddepcontrol.wait before touching global memory, so their prologue overlaps
+// the previous kernel's tail and the launch latency is hidden (sm100_ptx.cuh).
+// EMU_PDL=0 launches them plainly (A/B measurements).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       Args... args)
+{
+    static const int pdl = env_int("EMU_PDL", 1, 0, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 int prefetch_distance()
 {
     static const int pf = [] {
@@ -301,7 +323,9 @@ emu_status run_gemm(int dev, int sms, int m, int n, int k, float alpha, const fl
     p.strideA = a_b ? strideA : 0; p.strideB = b_b ? strideB : 0;
 
     const long long grid = std::min<long long>(p.num_tiles, sms);
-    emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE, LDG><<<(unsigned)grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+    const cudaError_t le = launch_pdl(emu::emu_sgemm_kernel<MODE, BN, ALAY, RANGE, LDG>, (unsigned)grid, Cfg::NUM_THREADS,
+                                      Cfg::SMEM_BYTES, stream, tmA, tmB, tmC, p);
+    if (le != cudaSuccess) return launch_status(le);
     g_last_launches = 1;
     g_last_kernel = kernel_name_once([](char* b, size_t nb) {
         snprintf(b, nb, "emu_sgemm_kernel<%s, BN=%d, A layout %d%s%s> (single CTA, M=128)", MODE == 0 ? "FP16" : "TF32",
@@ -372,8 +396,9 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     const long long clusters = std::min<long long>(p.num_tiles, sms / 2);
-    emu::emu_sgemm_pair_kernel<MODE, ALAY, RANGE>
-        <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+    const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_kernel<MODE, ALAY, RANGE>, (unsigned)(2 * clusters),
+                                      Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream, tmA, tmB, tmC, p);
+    if (le != cudaSuccess) return launch_status(le);
     g_last_launches = 1;
     g_last_kernel = kernel_name_once([](char* b, size_t nb) {
         snprintf(b, nb, "emu_sgemm_pair_kernel<%s, A layout %d%s> (CTA pair, both operands in SMEM)",
@@ -476,15 +501,19 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     bool launched = false;
     if constexpr (!RANGE && !TA && !TB) {
         if (p.num_dst > 1) {
-            emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true>
-                <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+            const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true>,
+                                              (unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream, tmA,
+                                              tmB, tmC, p);
+            if (le != cudaSuccess) return launch_status(le);
             launched = true;
         }
     }
     if (!launched) {
         if (p.num_dst > 1) return EMU_STATUS_NOT_SUPPORTED;
-        emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>
-            <<<(unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, p);
+        const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>,
+                                          (unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream, tmA, tmB,
+                                          tmC, p);
+        if (le != cudaSuccess) return launch_status(le);
     }
     g_last_launches = 1;
     g_last_kernel = kernel_name_once([](char* b, size_t nb) {

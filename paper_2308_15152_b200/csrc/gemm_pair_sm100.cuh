@@ -133,6 +133,7 @@ emu_sgemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_cons
     ptx::cluster_sync();   // barriers initialised and TMEM allocated in both CTAs
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    ptx::pdl_wait_then_allow_next();   // prologue done: wait for the previous kernel on the stream
 
     const int nks = p.num_k_stages;
     const int nkb = (nks + p.kb_stages - 1) / p.kb_stages;

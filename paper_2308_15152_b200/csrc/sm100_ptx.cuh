@@ -374,6 +374,20 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// -------------------------------------------- programmatic dependent launch
+// Launched with programmatic stream serialization (api.cu launch_pdl), a kernel may
+// start while the previous kernel on the stream is still running: its prologue
+// (barriers, TMEM allocation, tensor-map prefetch) overlaps that kernel's tail.
+// griddepcontrol.wait blocks until the previous grid has completed and its memory
+// is visible -- every thread calls it before its first global-memory access.
+// launch_dependents lets the NEXT kernel's launch proceed early (its CTAs still
+// need free SMs, and wait in turn).  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait_then_allow_next()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------ descriptors
 // UMMA shared-memory matrix descriptor (sm_100 "version 1" format):
 //   [0,14) start address >> 4, [16,30) leading byte offset >> 4,
