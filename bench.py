@@ -99,6 +99,7 @@ def _args():
     ap.add_argument("--mode", default="fp16", choices=["fp16", "tf32"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--kblock", type=int, default=0, help="combine interval KB (0 = the library default, R#7)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false",
@@ -397,6 +398,9 @@ def measure(args, cfg_name, mode, rank, world, local, steps, warmup, e2e=True, c
         if use_range:
             emu.emu_sgemm_batched_range(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, ws,
                                         ws_bytes, stream)
+        elif args.kblock:
+            emu.emu_sgemm_batched_ex(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, stream,
+                                     None, args.kblock, 0)
         else:
             emu.emu_sgemm_batched(m, n, k, 1.0, dA, m, sA, dB, k, sB, 0.0, dC, m, sC, batch, mode, stream)
         launches += emu.emu_last_launch_count()

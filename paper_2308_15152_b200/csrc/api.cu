@@ -66,7 +66,6 @@ struct DeviceInfo {
     int sms = 0;
     bool attr_set[32] = {};
     bool pair_attr_set[16] = {};
-    bool ts_attr_set[512] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -407,28 +406,28 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
-template <int MODE, int RANGE, int BN, bool SPLITC, bool ASTAT, bool TA = false, bool TB = false>
+template <int MODE, int RANGE, int BN, bool SPLITC, bool ASTAT, bool TA = false, bool TB = false, bool LONGK = false>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
                          unsigned flags, const unsigned* row_max, const unsigned* col_max)
 {
-    using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT>;
+    using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT, LONGK>;
     {
+        // the dynamic shared-memory attribute, once per device and instantiation
+        static bool attr_set[64] = {};
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        const int slot = (((((MODE * 4 + RANGE) * 3 + (BN == 96 ? 0 : BN == 128 ? 1 : 2)) * 2 + (SPLITC ? 1 : 0)) * 2 +
-                           (ASTAT ? 1 : 0)) * 2 + (TA ? 1 : 0)) * 2 + (TB ? 1 : 0);
-        if (!g_dev[dev].ts_attr_set[slot]) {
-            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>,
+        if (!attr_set[dev]) {
+            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, false, LONGK>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
                 return EMU_STATUS_CUDA_ERROR;
             if constexpr (!RANGE && !TA && !TB) {
-                if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true>,
+                if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true, LONGK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Cfg::SMEM_BYTES) != cudaSuccess)
                     return EMU_STATUS_CUDA_ERROR;
             }
-            g_dev[dev].ts_attr_set[slot] = true;
+            attr_set[dev] = true;
         }
     }
     const bool a_b = batch > 1 && strideA != 0;
@@ -453,6 +452,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     int tma_store = beta == 0.0f && aligned16(C) && ldc % 4 == 0 && (!c_b || strideC % 4 == 0) &&
                     (unsigned long long)strideC * 4 < (1ull << 40);
     if (g_mdst && g_mdst->n > 1) tma_store = 0;   // multicast: st.global to every destination
+    if (Cfg::CSTAGE_BYTES == 0) tma_store = 0;     // long-k variant: no C staging area
     if (tma_store) {
         const uint64_t sC = c_b ? (uint64_t)strideC : (((uint64_t)ldc * (uint64_t)n + 3) & ~uint64_t(3));
         // one 32-row x ECOLS block per combine warp (each warp stores its own columns)
@@ -501,7 +501,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     bool launched = false;
     if constexpr (!RANGE && !TA && !TB) {
         if (p.num_dst > 1) {
-            const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true>,
+            const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true, LONGK>,
                                               (unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream, tmA,
                                               tmB, tmC, p);
             if (le != cudaSuccess) return launch_status(le);
@@ -510,15 +510,16 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     }
     if (!launched) {
         if (p.num_dst > 1) return EMU_STATUS_NOT_SUPPORTED;
-        const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB>,
+        const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, false, LONGK>,
                                           (unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream, tmA, tmB,
                                           tmC, p);
         if (le != cudaSuccess) return launch_status(le);
     }
     g_last_launches = 1;
     g_last_kernel = kernel_name_once([](char* b, size_t nb) {
-        snprintf(b, nb, "emu_sgemm_pair_ts_kernel<%s, %d cols%s%s%s%s%s%s> (CTA pair, A in TMEM)",
+        snprintf(b, nb, "emu_sgemm_pair_ts_kernel<%s, %d cols%s%s%s%s%s%s%s> (CTA pair, A in TMEM)",
                  MODE == 0 ? "FP16" : "TF32", BN, SPLITC ? ", split commit" : "", ASTAT ? ", A-stationary" : "",
+                 Cfg::LONGK ? ", long-k rings" : "",
                  (RANGE & 2) ? ", range-safe" : "", (RANGE & 1) ? ", range flag" : "", TA ? ", op(A)=T" : "",
                  TB ? ", op(B)=T" : "");
     });
@@ -670,12 +671,19 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
                                                  : emu::PairTsCfg<1, 128, true, true>::ASLOTS;
     const bool ts_as = ts_sc && ts_as_env && (k + 31) / 32 <= ts_aslots && (n + 127) / 128 >= 2 &&
                        ts_units >= 2LL * (sms / 2);
+    // long k, streaming tiles: deeper operand / FP32 rings instead of the C staging area
+    static const int ts_lk_env = env_int("EMU_TS_LONGK", 1, 0, 1);   // tuning only (default on)
+    const bool ts_lk = ts_sc && !ts_as && ts_lk_env && (k + 31) / 32 >= 64;
 #define EMU_RUN_TS(MODE_, RANGE_)                                                                                      \
     do {                                                                                                               \
         if (ts_as)                                                                                                     \
             { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, \
                                                                     strideB, beta, C, ldc, strideC, batch, s,          \
                                                                     d_range_flag, kblock, flags, row_max, col_max); break; }    \
+        if (ts_lk)                                                                                                     \
+            { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, false, false, false, true>(dev, sms, m, n, k, alpha, A,  \
+                                     lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, s, d_range_flag,     \
+                                     kblock, flags, row_max, col_max); break; }                                        \
         if (ts_sc)                                                                                                     \
             { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, false>(dev, sms, m, n, k, alpha, A, lda, strideA, B,     \
                                                                      ldb, strideB, beta, C, ldc, strideC, batch, s,    \

@@ -38,8 +38,12 @@
 
 namespace emu {
 
-template <int MODE, int BN_ = 128, bool SPLITC_ = true, bool ASTAT_ = false>
+// LONGK_ (long-k streaming tiles, c3): no C staging area (the epilogue stores with
+// st.global -- once per tile, negligible at long k), its 64 KB spent on deeper rings:
+// FP16 8 operand slots (a whole KB = 128 k-block plus half of the next) and 6 FP32 stages
+template <int MODE, int BN_ = 128, bool SPLITC_ = true, bool ASTAT_ = false, bool LONGK_ = false>
 struct PairTsCfg {
+    static constexpr bool LONGK = LONGK_ && !ASTAT_;
     static constexpr int BM = 128;                      // A rows per CTA (pair M = 256)
     static constexpr int BN = BN_;                      // pair tile N = D columns per CTA
     static constexpr int BNC = BN / 2;                  // B columns staged per CTA
@@ -55,7 +59,7 @@ struct PairTsCfg {
     static constexpr uint32_t F32_STAGE = A32_BYTES + B32_BYTES;
     static constexpr uint32_t BOP_BYTES = BNC * BK * ESZ;  // one of B_hi / B_lo
     static constexpr uint32_t OP_STAGE = 2 * BOP_BYTES;
-    static constexpr uint32_t CSTAGE_BYTES = BM * BN * 4;  // TMA-store staging (48 / 64 KB)
+    static constexpr uint32_t CSTAGE_BYTES = LONGK ? 0 : BM * BN * 4;  // TMA-store staging (48 / 64 KB)
     static constexpr uint32_t B_ROW = BK * ESZ;            // 64 (FP16) / 128 (TF32) bytes
     static constexpr uint32_t B_SBO = 8 * B_ROW;
     static constexpr uint32_t B_LAYOUT = MODE == 0 ? 4 : 2;
@@ -67,11 +71,12 @@ struct PairTsCfg {
     static constexpr int ASLOTS = (TMEM_COLS - A_COL0) / ACOLS;   // A stages TMEM holds
     // operand ring: B_hi/B_lo in shared memory (and the A stage in TMEM unless ASTAT);
     // FP16: 5 slots still leave room for 5 FP32 stages
-    static constexpr int SOP_MAX = MODE == 0 ? 5 : 4;
+    static constexpr int SOP_MAX = MODE == 0 ? (LONGK ? 8 : 5) : 4;
     static constexpr int SOP = ASLOTS < SOP_MAX ? ASLOTS : SOP_MAX;
     // FP32 stages: as many as fit next to the operand ring and C staging (<= 5)
     static constexpr int S32_FIT = (232448 - 2048 - SOP * OP_STAGE - CSTAGE_BYTES) / F32_STAGE;
-    static constexpr int S32 = S32_FIT < 5 ? S32_FIT : 5;
+    static constexpr int S32_MAX = LONGK ? 6 : 5;
+    static constexpr int S32 = S32_FIT < S32_MAX ? S32_FIT : S32_MAX;
     static constexpr uint32_t KCOLS = 8;                       // TMEM columns per MMA K step
     static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
     static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4 + ASLOTS) + 16;
@@ -116,12 +121,13 @@ __device__ __forceinline__ void ts_unit_tile(const GemmParams& p, long long u, i
 // RANGE (bit mask): 1 compiles in the FP16 overflow flag (p.range_flag), 2 the range-safe
 // mode's power-of-two scaling (p.row_max / p.col_max, R#22); each still enabled by its pointer.
 // MC: epilogue stores every tile to p.dst[0 .. num_dst-1] (fused all-gather, NEXT row 3)
-template <int MODE, int RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false, bool MC = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, SPLITC_, ASTAT_>::NUM_THREADS, 1)
+template <int MODE, int RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false, bool MC = false,
+          bool LONGK_ = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, SPLITC_, ASTAT_, LONGK_>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const GemmParams p)
 {
-    using Cfg = PairTsCfg<MODE, BN, SPLITC_, ASTAT_>;
+    using Cfg = PairTsCfg<MODE, BN, SPLITC_, ASTAT_, LONGK_>;
     constexpr bool ASTAT = Cfg::ASTAT;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
