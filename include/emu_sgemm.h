@@ -64,6 +64,15 @@ typedef enum {
                                       correction products; a negative control only */
 #define EMU_FLAG_SIMT 2u           /* emu_tcec_* only: the device API's "simt" backend,
                                       the same three products on CUDA cores, for evaluation */
+#define EMU_FLAG_PIPELINED 4u      /* emu_tcec_gemm_batched / emu_tcec_householder_batched only: the
+                                      pipelined (warp-specialized) form of the device API
+                                      (include/emu_tcec_pipeline.cuh) instead of the synchronous
+                                      tile -- the library's kernel with the caller's operand hooks.
+                                      Tensor-core backend only (with EMU_FLAG_SIMT ->
+                                      EMU_STATUS_NOT_SUPPORTED); FP32 operands read from memory must
+                                      be in the TMA domain (16-byte aligned, ld and stride multiples
+                                      of 4) else EMU_STATUS_NOT_SUPPORTED.  Same results as
+                                      emu_sgemm_batched_ex with the same kblock, bit for bit. */
 
 /*
  * emu_sgemm_batched -- C_b = alpha * A_b B_b + beta * C_b for b in [0, batch).

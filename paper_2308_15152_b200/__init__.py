@@ -16,7 +16,7 @@ __all__ = [
     "EMU_SPLIT_FP16", "EMU_SPLIT_TF32", "EMU_FLAG_NO_CORRECTION", "EmuError", "lib", "LIB_PATH",
     "emu_sgemm", "emu_sgemm_batched", "emu_sgemm_batched_ex", "emu_sgemm_batched_host",
     "emu_split", "emu_status_string", "emu_version", "emu_last_launch_count", "emu_last_kernel_name", "mode_of",
-    "EMU_FLAG_SIMT", "emu_tcec_gemm_batched", "emu_tcec_householder_batched", "emu_tcec_givens_batched",
+    "EMU_FLAG_SIMT", "EMU_FLAG_PIPELINED", "emu_tcec_gemm_batched", "emu_tcec_householder_batched", "emu_tcec_givens_batched",
     "emu_tcec_scan", "emu_sgemm_multicast", "EMU_COL_MAJOR", "EMU_ROW_MAJOR", "emu_sgemm_batched_layout",
     "matmul",
 ]
@@ -27,6 +27,7 @@ EMU_SPLIT_FP16 = 0
 EMU_SPLIT_TF32 = 1
 EMU_FLAG_NO_CORRECTION = 1
 EMU_FLAG_SIMT = 2
+EMU_FLAG_PIPELINED = 4
 EMU_COL_MAJOR = 0
 EMU_ROW_MAJOR = 1
 STATUS = {0: "SUCCESS", 1: "INVALID_VALUE", 2: "NOT_SUPPORTED", 3: "ARCH_MISMATCH",

@@ -218,6 +218,13 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, long long count, 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// an FP32 operand the TMA path can read: 16-byte aligned base, leading dimension and
+// batch stride in 16-byte units
+bool tma_domain(const float* X, long long ld, long long stride)
+{
+    return aligned16(X) && ld % 4 == 0 && stride % 4 == 0;
+}
+
 // L2 prefetch distance (k-stages) of the TMA producer; EMU_PREFETCH overrides (tuning only)
 int env_int(const char* name, int dflt, int lo, int hi)
 {
@@ -406,11 +413,12 @@ emu_status run_gemm_pair(int dev, int sms, int m, int n, int k, float alpha, con
     return launch_status(cudaGetLastError());
 }
 
-template <int MODE, int RANGE, int BN, bool SPLITC, bool ASTAT, bool TA = false, bool TB = false, bool LONGK = false>
+template <int MODE, int RANGE, int BN, bool SPLITC, bool ASTAT, bool TA = false, bool TB = false, bool LONGK = false,
+          class Ops = emu::lib_operands>
 emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
                          long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                          long long strideC, int batch, cudaStream_t stream, unsigned* range_flag, int kblock,
-                         unsigned flags, const unsigned* row_max, const unsigned* col_max)
+                         unsigned flags, const unsigned* row_max, const unsigned* col_max, const Ops& ops = Ops())
 {
     using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT, LONGK>;
     {
@@ -418,11 +426,11 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
         static bool attr_set[64] = {};
         std::lock_guard<std::mutex> lk(g_dev_mu);
         if (!attr_set[dev]) {
-            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, false, LONGK>,
+            if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, false, LONGK, Ops>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES) != cudaSuccess)
                 return EMU_STATUS_CUDA_ERROR;
             if constexpr (!RANGE && !TA && !TB) {
-                if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true, LONGK>,
+                if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true, LONGK, Ops>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Cfg::SMEM_BYTES) != cudaSuccess)
                     return EMU_STATUS_CUDA_ERROR;
@@ -440,11 +448,12 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     const uint64_t sA = a_b ? (uint64_t)strideA : (((uint64_t)lda * (uint64_t)(TA ? m : k) + 3) & ~uint64_t(3));
     const uint64_t sB = b_b ? (uint64_t)strideB : (((uint64_t)ldb * (uint64_t)(TB ? k : n) + 3) & ~uint64_t(3));
     // op(A) = A (m x k, m contiguous) or A^T (A stored k x m); op(B) = B (k x n) or B^T (B stored n x k)
-    const bool mapA = TA ? make_map(&tmA, A, (uint64_t)k, (uint64_t)m, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA,
+    // generated operands (Ops::gen_a / gen_b) need no tensor map
+    const bool mapA = Ops::gen_a ? true : TA ? make_map(&tmA, A, (uint64_t)k, (uint64_t)m, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA,
                                     Cfg::BK, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_128B)
                          : make_map(&tmA, A, (uint64_t)m, (uint64_t)k, (uint64_t)lda, a_b ? (uint64_t)batch : 1, sA,
                                     Cfg::BM, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE);
-    const bool mapB = TB ? make_map(&tmB, B, (uint64_t)n, (uint64_t)k, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB,
+    const bool mapB = Ops::gen_b ? true : TB ? make_map(&tmB, B, (uint64_t)n, (uint64_t)k, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB,
                                     Cfg::BNC, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
                          : make_map(&tmB, B, (uint64_t)k, (uint64_t)n, (uint64_t)ldb, b_b ? (uint64_t)batch : 1, sB,
                                     Cfg::BK, Cfg::BNC, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -453,6 +462,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
                     (unsigned long long)strideC * 4 < (1ull << 40);
     if (g_mdst && g_mdst->n > 1) tma_store = 0;   // multicast: st.global to every destination
     if (Cfg::CSTAGE_BYTES == 0) tma_store = 0;     // long-k variant: no C staging area
+    if (Ops::custom_store) tma_store = 0;          // the user's epilogue stores
     if (tma_store) {
         const uint64_t sC = c_b ? (uint64_t)strideC : (((uint64_t)ldc * (uint64_t)n + 3) & ~uint64_t(3));
         // one 32-row x ECOLS block per combine warp (each warp stores its own columns)
@@ -501,18 +511,18 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     bool launched = false;
     if constexpr (!RANGE && !TA && !TB) {
         if (p.num_dst > 1) {
-            const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true, LONGK>,
+            const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, true, LONGK, Ops>,
                                               (unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream, tmA,
-                                              tmB, tmC, p);
+                                              tmB, tmC, p, ops);
             if (le != cudaSuccess) return launch_status(le);
             launched = true;
         }
     }
     if (!launched) {
         if (p.num_dst > 1) return EMU_STATUS_NOT_SUPPORTED;
-        const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, false, LONGK>,
+        const cudaError_t le = launch_pdl(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, false, LONGK, Ops>,
                                           (unsigned)(2 * clusters), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream, tmA, tmB,
-                                          tmC, p);
+                                          tmC, p, ops);
         if (le != cudaSuccess) return launch_status(le);
     }
     g_last_launches = 1;
@@ -525,6 +535,57 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     });
     if (launched) g_last_kernel = "emu_sgemm_pair_ts_kernel<multicast epilogue> (CTA pair, A in TMEM)";
     return launch_status(cudaGetLastError());
+}
+
+// TS-kernel variant for a problem (shared by the library entries and the pipelined
+// device-API entries): tile width, split commit, A-stationary, long-k rings
+struct TsPlan {
+    int n;
+    bool sc, as, lk;
+};
+
+TsPlan ts_plan(int mode, int m, int n, int k, int batch, int sms, bool multicast)
+{
+    static const int ts_n_env = env_int("EMU_TS_N", 0, 0, 128);   // tuning only
+    // few tiles (fewer 256 x 128 tiles than clusters, e.g. c4's 1024^2 output): 64-wide
+    // tiles with double-buffered accumulators put twice as many clusters to work
+    const long long ts_tiles128 = (long long)((m + 255) / 256) * ((n + 127) / 128) * batch;
+    TsPlan t;
+    t.n = ts_n_env ? ts_n_env : (ts_tiles128 < sms / 2 && n > 64 && !multicast ? 64 : 128);
+    static const int ts_sc_env = env_int("EMU_TS_SPLITC", 1, 0, 1);   // tuning only (default on)
+    static const int ts_as_env = env_int("EMU_TS_ASTAT", 1, 0, 1);    // tuning only (default on)
+    t.sc = t.n == 128 && ts_sc_env;
+    // A-stationary: all of k fits the TMEM A slots, at least two n-tiles share the split
+    // A, and there are enough (batch, m-pair) row blocks to keep every cluster busy
+    const long long ts_units = (long long)((m + 255) / 256) * batch;
+    const int ts_aslots = mode == EMU_SPLIT_FP16 ? emu::PairTsCfg<0, 128, true, true>::ASLOTS
+                                                 : emu::PairTsCfg<1, 128, true, true>::ASLOTS;
+    t.as = t.sc && ts_as_env && (k + 31) / 32 <= ts_aslots && (n + 127) / 128 >= 2 && ts_units >= 2LL * (sms / 2);
+    // long k, streaming tiles: deeper operand / FP32 rings instead of the C staging area
+    static const int ts_lk_env = env_int("EMU_TS_LONGK", 1, 0, 1);   // tuning only (default on)
+    t.lk = t.sc && !t.as && ts_lk_env && (k + 31) / 32 >= 64;
+    return t;
+}
+
+// the pipelined (warp-specialized) form of the device API (include/emu_tcec_pipeline.cuh):
+// the library's TS kernel with the caller's operand / epilogue hooks (no range mode,
+// no transposes; column-major, alpha / beta as the library)
+template <int MODE, class Ops>
+emu_status run_pipelined(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
+                         long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
+                         long long strideC, int batch, cudaStream_t s, int kblock, unsigned flags, const Ops& ops)
+{
+    const TsPlan t = ts_plan(MODE, m, n, k, batch, sms, false);
+#define EMU_RUN_P(BN_, SC_, AS_, LK_)                                                                            \
+    return run_gemm_pair_ts<MODE, 0, BN_, SC_, AS_, false, false, LK_, Ops>(                                     \
+        dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, s, nullptr,    \
+        kblock, flags, nullptr, nullptr, ops)
+    if (t.as) EMU_RUN_P(128, true, true, false);
+    if (t.lk) EMU_RUN_P(128, true, false, true);
+    if (t.sc) EMU_RUN_P(128, true, false, false);
+    if (t.n == 64) EMU_RUN_P(64, false, false, false);
+    EMU_RUN_P(128, false, false, false);
+#undef EMU_RUN_P
 }
 
 }  // namespace
@@ -568,6 +629,7 @@ static int default_kblock(int k)
 }
 
 // the device entries; range_ws != nullptr selects the range-safe mode (R#22)
+
 static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, int lda, long long strideA,
                             const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
                             long long strideC, int batch, emu_split_mode mode, void* stream,
@@ -656,24 +718,9 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     // buffer whose D_corr and D_hi drains overlap the other part's MMAs (SPLITC); the
     // double-buffered 96-wide tile (EMU_TS_N=96) and the plain single buffer
     // (EMU_TS_SPLITC=0) stay selectable for comparison.
-    static const int ts_n_env = env_int("EMU_TS_N", 0, 0, 128);   // tuning only
-    // few tiles (fewer 256 x 128 tiles than clusters, e.g. c4's 1024^2 output): 64-wide
-    // tiles with double-buffered accumulators put twice as many clusters to work
-    const long long ts_tiles128 = (long long)((m + 255) / 256) * ((n + 127) / 128) * batch;
-    const int ts_n = ts_n_env ? ts_n_env : (ts_tiles128 < sms / 2 && n > 64 && !g_mdst ? 64 : 128);
-    static const int ts_sc_env = env_int("EMU_TS_SPLITC", 1, 0, 1);   // tuning only (default on)
-    static const int ts_as_env = env_int("EMU_TS_ASTAT", 1, 0, 1);    // tuning only (default on)
-    const bool ts_sc = ts_n == 128 && ts_sc_env;
-    // A-stationary: all of k fits the TMEM A slots, at least two n-tiles share the split
-    // A, and there are enough (batch, m-pair) row blocks to keep every cluster busy
-    const long long ts_units = (long long)((m + 255) / 256) * batch;
-    const int ts_aslots = mode == EMU_SPLIT_FP16 ? emu::PairTsCfg<0, 128, true, true>::ASLOTS
-                                                 : emu::PairTsCfg<1, 128, true, true>::ASLOTS;
-    const bool ts_as = ts_sc && ts_as_env && (k + 31) / 32 <= ts_aslots && (n + 127) / 128 >= 2 &&
-                       ts_units >= 2LL * (sms / 2);
-    // long k, streaming tiles: deeper operand / FP32 rings instead of the C staging area
-    static const int ts_lk_env = env_int("EMU_TS_LONGK", 1, 0, 1);   // tuning only (default on)
-    const bool ts_lk = ts_sc && !ts_as && ts_lk_env && (k + 31) / 32 >= 64;
+    const TsPlan plan = ts_plan(mode, m, n, k, batch, sms, g_mdst != nullptr);
+    const int ts_n = plan.n;
+    const bool ts_sc = plan.sc, ts_as = plan.as, ts_lk = plan.lk;
 #define EMU_RUN_TS(MODE_, RANGE_)                                                                                      \
     do {                                                                                                               \
         if (ts_as)                                                                                                     \

@@ -116,16 +116,33 @@ __device__ __forceinline__ void ts_unit_tile(const GemmParams& p, long long u, i
     }
 }
 
+// Operand and epilogue hooks of the kernel (the pipelined form of the device API,
+// include/emu_tcec_pipeline.cuh).  The library's own GEMMs use these defaults: both
+// FP32 operands come from global memory through TMA, the epilogue is the library's
+// C = alpha * C_acc + beta * C_old store.  A user type replaces either operand by a
+// rule evaluated by the splitter warps (foreach_ij; the operand never
+// exists in memory) and / or the store:
+//   gen_a:  __device__ float a(int batch, int i, int p) const   A_b(i, p), i < m, p < k
+//   gen_b:  __device__ float b(int batch, int p, int j) const   B_b(p, j), p < k, j < n
+//   custom_store: __device__ void store(int batch, int i, int j0, const float* c, int cols) const
+//           C_b(i, j0 + jj) from the FP32 accumulator c[jj], jj < cols (i < m, j0 + jj < n)
+struct lib_operands {
+    static constexpr bool gen_a = false, gen_b = false, custom_store = false;
+    __device__ float a(int, int, int) const { return 0.0f; }
+    __device__ float b(int, int, int) const { return 0.0f; }
+    __device__ void store(int, int, int, const float*, int) const {}
+};
+
 // TA / TB: op(A) = A^T (A stored k x m, k contiguous) / op(B) = B^T (B stored n x k):
 // only the TMA boxes and the splitters' shared-memory reads change (NEXT row 2)
 // RANGE (bit mask): 1 compiles in the FP16 overflow flag (p.range_flag), 2 the range-safe
 // mode's power-of-two scaling (p.row_max / p.col_max, R#22); each still enabled by its pointer.
 // MC: epilogue stores every tile to p.dst[0 .. num_dst-1] (fused all-gather, NEXT row 3)
 template <int MODE, int RANGE, int BN, bool SPLITC_, bool ASTAT_, bool TA = false, bool TB = false, bool MC = false,
-          bool LONGK_ = false>
+          bool LONGK_ = false, class Ops = lib_operands>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairTsCfg<MODE, BN, SPLITC_, ASTAT_, LONGK_>::NUM_THREADS, 1)
 emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         const __grid_constant__ CUtensorMap tmC, const GemmParams p)
+                         const __grid_constant__ CUtensorMap tmC, const GemmParams p, const Ops ops = Ops())
 {
     using Cfg = PairTsCfg<MODE, BN, SPLITC_, ASTAT_, LONGK_>;
     constexpr bool ASTAT = Cfg::ASTAT;
@@ -171,8 +188,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         }
         for (int i = 0; i < Cfg::ASLOTS; ++i) ptx::mbar_init(&aslot_empty[i], 1);
         ptx::fence_mbar_init();
-        ptx::prefetch_tmap(&tmA);
-        ptx::prefetch_tmap(&tmB);
+        if (!Ops::gen_a) ptx::prefetch_tmap(&tmA);
+        if (!Ops::gen_b) ptx::prefetch_tmap(&tmB);
     }
     if (warp == 1) ptx::tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
     ptx::tc_fence_before();
@@ -210,8 +227,13 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                             PROF_ADD(P_PROD_WAIT_EMPTY);
                             uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                             TRACE_AT(0, 1, ks);
-                            ptx::mbar_arrive_expect_tx(&f32_full[s], loadA ? Cfg::F32_STAGE : Cfg::B32_BYTES);
-                            if (loadA) {
+                            // generated operands (Ops::gen_a / gen_b) are not loaded: the splitter
+                            // warps evaluate them
+                            const uint32_t bytes = (loadA && !Ops::gen_a ? Cfg::A32_BYTES : 0u) +
+                                                   (Ops::gen_b ? 0u : Cfg::B32_BYTES);
+                            if (bytes) ptx::mbar_arrive_expect_tx(&f32_full[s], bytes);
+                            else ptx::mbar_arrive(&f32_full[s]);
+                            if (loadA && !Ops::gen_a) {
                                 if (TA)   // [128 m][32 k], SWIZZLE_128B rows
                                     load(dst, &tmA, &f32_full[s], ks * Cfg::BK, mt * 256 + rank * Cfg::BM, ab,
                                          hint_a, pol_a);
@@ -219,7 +241,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                     load(dst, &tmA, &f32_full[s], mt * 256 + rank * Cfg::BM, ks * Cfg::BK, ab,
                                          hint_a, pol_a);
                             }
-                            if (TB)       // [32 k][BN/2 n]
+                            if (Ops::gen_b) {
+                            } else if (TB)   // [32 k][BN/2 n]
                                 load(dst + Cfg::A32_BYTES, &tmB, &f32_full[s], nt * Cfg::BN + rank * Cfg::BNC,
                                      ks * Cfg::BK, bb, hint_b, pol_b);
                             else          // [BN/2 n][32 k], SWIZZLE_128B rows
@@ -422,6 +445,14 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         for (long long u = cid; u < num_units; u += ncl, ++unit_it) {
             for (int j = 0; j < R; ++j) {
                 const bool doA = !ASTAT || j == 0;
+                // generated operands: this thread's problem, row of A and column of B
+                int gb = 0, grow = 0, gcol = 0;
+                if (Ops::gen_a || Ops::gen_b) {
+                    int mt_, nt_;
+                    ts_unit_tile<ASTAT>(p, u, j, gb, mt_, nt_);
+                    grow = mt_ * 256 + (int)rank * Cfg::BM + (int)m;
+                    gcol = nt_ * Cfg::BN + (int)rank * Cfg::BNC + (int)n;
+                }
                 // range-safe mode: this thread's row of A and column of B scale by 2^-e
                 float sa = 1.0f, sb = 1.0f;
                 if ((RANGE & 2) && p.row_max) {
@@ -453,7 +484,12 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     // ---- load phase: A(m, KS kq .. +KS-1) (a warp reads 32 consecutive m per k),
                     //      B(8 quarter .. +7, n): FP32 16-byte chunks 2 quarter, 2 quarter + 1 of row n
                     float av[Cfg::KS];
-                    if (doA && TA) {
+                    if (doA && Ops::gen_a) {
+                        const int k0 = ks * Cfg::BK + (int)kq * Cfg::KS;
+#pragma unroll
+                        for (int jj = 0; jj < Cfg::KS; ++jj)
+                            av[jj] = (grow < p.m && k0 + jj < p.k) ? ops.a(gb, grow, k0 + jj) : 0.0f;
+                    } else if (doA && TA) {
                         // row m holds 32 k (128 bytes, 16-byte chunks XOR-swizzled by m & 7)
                         const uint8_t* ra = reinterpret_cast<const uint8_t*>(fa) + m * 128;
 #pragma unroll
@@ -467,7 +503,14 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         for (int jj = 0; jj < Cfg::KS; ++jj) av[jj] = fa[(kq * Cfg::KS + jj) * Cfg::BM + m];
                     }
                     float4 vb[2];
-                    if (has_b && TB) {
+                    if (has_b && Ops::gen_b) {
+                        const int k0 = ks * Cfg::BK + (int)quarter * 8;
+                        float x[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) x[i] = (gcol < p.n && k0 + i < p.k) ? ops.b(gb, k0 + i, gcol) : 0.0f;
+                        vb[0] = make_float4(x[0], x[1], x[2], x[3]);
+                        vb[1] = make_float4(x[4], x[5], x[6], x[7]);
+                    } else if (has_b && TB) {
                         // k-row of BN/2 columns: a warp reads 32 consecutive n per k
                         const float* fbt = reinterpret_cast<const float*>(fb);
                         float x[8];
@@ -705,7 +748,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         creg[jj] = ldexp_rn(creg[jj], er + fc);
                     }
                 }
-                if (p.tma_store) {
+                if (Ops::custom_store) {
+                    const int r = mrow0 + (int)(q * 32 + lane);
+                    const int col0 = nt * Cfg::BN + (int)(h * HALF);
+                    if (r < p.m) ops.store(b, r, col0, creg, min(HALF, p.n - col0));
+                } else if (p.tma_store) {
                     // each warp stages and TMA-stores its own 32 rows x HALF columns (no
                     // CTA-wide barrier: a warp moves on to the next tile's drains at once)
                     float* dst = cstage + e * (32 * HALF);

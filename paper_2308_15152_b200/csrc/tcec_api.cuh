@@ -6,6 +6,7 @@
 #pragma once
 
 #include "emu_tcec.cuh"
+#include "emu_tcec_pipeline.cuh"
 
 namespace emu {
 namespace tcec_kernels {
@@ -87,6 +88,21 @@ __device__ __forceinline__ float householder_elem(float vi, float vp, bool diag)
     const float e = __fmul_rn(__fmul_rn(vi, vp), -2.0f);
     return diag ? __fadd_rn(e, 1.0f) : e;
 }
+
+// the same operand for the pipelined form (include/emu_tcec_pipeline.cuh): the
+// library's warp-specialized kernel evaluates H(i, p) in its splitter warps
+struct householder_operands {
+    static constexpr bool gen_a = true, gen_b = false, custom_store = false;
+    const float* V;
+    long long strideV;
+    __device__ float a(int b, int i, int p) const
+    {
+        const float* v = V + b * strideV;
+        return householder_elem(__ldg(v + i), __ldg(v + p), i == p);
+    }
+    __device__ float b(int, int, int) const { return 0.0f; }
+    __device__ void store(int, int, int, const float*, int) const {}
+};
 
 template <class Pol, int N>
 __global__ void __launch_bounds__(128) tcec_householder_kernel(const HouseArgs a)
@@ -205,7 +221,7 @@ using emu::tcec::without_ec;
 using emu::tcec::tensor_core;
 using emu::tcec::simt;
 
-constexpr unsigned kTcecFlags = EMU_FLAG_NO_CORRECTION | EMU_FLAG_SIMT;
+constexpr unsigned kTcecFlags = EMU_FLAG_NO_CORRECTION | EMU_FLAG_SIMT | EMU_FLAG_PIPELINED;
 
 // launch `Kern<Pol, N>` for the policy the (mode, flags) pair selects; N = 64
 // on the tensor cores (two CTAs' operand rings and TMEM fit one SM), 32 on SIMT
@@ -309,6 +325,18 @@ __attribute__((visibility("default"))) emu_status emu_tcec_gemm_batched(
         g_last_launches = 1;
         return launch_status(cudaGetLastError());
     }
+    if (flags & EMU_FLAG_PIPELINED) {   // the warp-specialized form (= the library kernel, default operands)
+        if (flags & EMU_FLAG_SIMT) return EMU_STATUS_NOT_SUPPORTED;
+        if (!tma_domain(A, lda, batch > 1 ? strideA : 0) || !tma_domain(B, ldb, batch > 1 ? strideB : 0))
+            return EMU_STATUS_NOT_SUPPORTED;
+        const int kb = kblock ? kblock : default_kblock(k);
+        const unsigned f = flags & EMU_FLAG_NO_CORRECTION;
+        return mode == EMU_SPLIT_FP16
+                   ? run_pipelined<0>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+                                      batch, s, kb, f, emu::lib_operands())
+                   : run_pipelined<1>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+                                      batch, s, kb, f, emu::lib_operands());
+    }
     emu::tcec_kernels::GemmArgs a{m, n, k, batch, alpha, beta, A, lda, batch > 1 ? strideA : 0, B, ldb,
                                   batch > 1 ? strideB : 0, C, ldc, strideC, kbs};
     dim3 g;
@@ -332,6 +360,18 @@ __attribute__((visibility("default"))) emu_status emu_tcec_householder_batched(
     int dev = 0, sms = 0;
     emu_status st = device_check(dev, sms);
     if (st != EMU_STATUS_SUCCESS) return st;
+    if (flags & EMU_FLAG_PIPELINED) {   // H generated by the library kernel's splitter warps
+        if (flags & EMU_FLAG_SIMT) return EMU_STATUS_NOT_SUPPORTED;
+        if (!tma_domain(X, ldx, batch > 1 ? strideX : 0)) return EMU_STATUS_NOT_SUPPORTED;
+        const emu::tcec_kernels::householder_operands ops{V, batch > 1 ? strideV : 0};
+        const unsigned f = flags & EMU_FLAG_NO_CORRECTION;
+        cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+        return mode == EMU_SPLIT_FP16
+                   ? run_pipelined<0>(dev, sms, m, n, m, 1.0f, nullptr, m, 0, X, ldx, strideX, 0.0f, C, ldc, strideC,
+                                      batch, s, 64, f, ops)
+                   : run_pipelined<1>(dev, sms, m, n, m, 1.0f, nullptr, m, 0, X, ldx, strideX, 0.0f, C, ldc, strideC,
+                                      batch, s, 64, f, ops);
+    }
     emu::tcec_kernels::HouseArgs a{m, n, batch, kbs, V, batch > 1 ? strideV : 0, X, ldx, batch > 1 ? strideX : 0,
                                    C, ldc, strideC};
     dim3 g;
@@ -350,6 +390,7 @@ __attribute__((visibility("default"))) emu_status emu_tcec_givens_batched(
     if (ldx < std::max(1, m) || ldc < std::max(1, m) || strideX < 0 || strideC < 0) return EMU_STATUS_INVALID_VALUE;
     if (m == 0 || n == 0 || batch == 0) return EMU_STATUS_SUCCESS;
     if (i < 0 || j < 0 || i >= m || j >= m || i == j) return EMU_STATUS_INVALID_VALUE;
+    if (flags & EMU_FLAG_PIPELINED) return EMU_STATUS_NOT_SUPPORTED;   // tile form only
     if (CS == nullptr || X == nullptr || C == nullptr) return EMU_STATUS_INVALID_VALUE;
     if (batch > 1 && strideC < (long long)ldc * n) return EMU_STATUS_INVALID_VALUE;
     int dev = 0, sms = 0;
@@ -372,6 +413,7 @@ __attribute__((visibility("default"))) emu_status emu_tcec_scan(int n, int count
     if (ldx < std::max(1, n) || ldy < std::max(1, n)) return EMU_STATUS_INVALID_VALUE;
     if (n == 0 || count == 0) return EMU_STATUS_SUCCESS;
     if (X == nullptr || Y == nullptr) return EMU_STATUS_INVALID_VALUE;
+    if (flags & EMU_FLAG_PIPELINED) return EMU_STATUS_NOT_SUPPORTED;   // tile form only
     int dev = 0, sms = 0;
     emu_status st = device_check(dev, sms);
     if (st != EMU_STATUS_SUCCESS) return st;

@@ -148,7 +148,7 @@ def test_tcec_entries_validation(emu):
     """device-API users (NEXT rows 2 and 4): argument checks run before any CUDA call"""
     L = emu.lib
     g = [8, 8, 8, 1.0, 16, 8, 0, 16, 8, 0, 0.0, 16, 8, 0, 1, 0, None]
-    assert L.emu_tcec_gemm_batched(*g, 0, 4) == 1            # unknown flag bit
+    assert L.emu_tcec_gemm_batched(*g, 0, 8) == 1            # unknown flag bit
     assert L.emu_tcec_gemm_batched(*g, 32, 0) == 1           # FP16 kblock below the 64-k stage
     assert L.emu_tcec_gemm_batched(*g, 96, 0) == 1           # not a multiple of 64
     assert L.emu_tcec_gemm_batched(*g, 0, 8) == 1

@@ -206,8 +206,56 @@ def test_tcec_argument_errors():
     import torch
     x = torch.zeros(64, device="cuda")
     with pytest.raises(emu.EmuError):
-        emu.emu_tcec_gemm_batched(8, 8, 8, 1.0, x, 8, 0, x, 8, 0, 0.0, x, 8, 0, 1, "fp16", None, 0, 4)
+        emu.emu_tcec_gemm_batched(8, 8, 8, 1.0, x, 8, 0, x, 8, 0, 0.0, x, 8, 0, 1, "fp16", None, 0, 8)
     with pytest.raises(emu.EmuError):
         emu.emu_tcec_gemm_batched(8, 8, 8, 1.0, x, 8, 0, x, 8, 0, 0.0, x, 8, 0, 1, "fp16", None, 32, 0)
     with pytest.raises(emu.EmuError):
         emu.emu_tcec_givens_batched(8, 1, 3, 3, x, x, 8, 0, x, 8, 0, 1, "fp16")
+
+
+# ------------------------------------------- pipelined (warp-specialized) form ----
+PIPE = 4   # EMU_FLAG_PIPELINED
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("shape", [(150, 256, 256, 256), (3, 300, 260, 320), (2, 100, 72, 2100)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_pipelined_gemm_is_the_library_kernel(mode, shape):
+    """emu_tcec_gemm_batched with EMU_FLAG_PIPELINED runs the library's warp-specialized
+    kernel through the device API's operand hooks: bit for bit the library's result
+    (same kblock) and the oracle's tensor-core model, with and without correction"""
+    from gpu_util import emu_gpu
+    batch, m, n, k = shape
+    A, B = workloads.make_operands(batch, m, n, k, seed=90 + k)
+    for flags in (PIPE, PIPE | NO_CORR):
+        C = _tcec_gemm(mode, A, B, m, n, k, flags=flags)
+        assert np.array_equal(C, emu_gpu(mode, A, B, m, n, k, flags=flags & NO_CORR)), flags
+        if batch <= 3:
+            assert_bits_equal(C, oracle.emu_gemm(mode, A, B, m, n, k, corr=not (flags & NO_CORR), tc="sm100"))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("shape", [(5, 32, 72), (160, 200, 256), (3, 256, 520)], ids=lambda s: "x".join(map(str, s)))
+def test_pipelined_householder(mode, shape):
+    """H generated by the library kernel's splitter warps (Ops::gen_a): the same bits
+    as the synchronous tile form and as the oracle on the explicit H"""
+    batch, m, n = shape
+    V = workloads.unit_vectors(batch, m, seed=170 + m)
+    _, X = workloads.make_operands(batch, n, n, m, seed=180 + m)
+    C = _householder(mode, V, X, m, n, flags=PIPE)
+    assert np.array_equal(C, _householder(mode, V, X, m, n))
+    for b in sorted({0, batch - 1}):
+        Hc = workloads.colmajor(structured.householder_matrix(V[b]))[None]
+        assert_bits_equal(C[b:b + 1], oracle.emu_gemm(mode, Hc, X[b:b + 1], m, n, m, tc="sm100"))
+        ref = oracle.emu_gemm(mode, Hc, X[b:b + 1], m, n, m)
+        assert np.all(np.abs(C[b:b + 1].astype(np.float64) - ref) <= tolerance(mode, Hc, X[b:b + 1], m, n, m, 64))
+
+
+def test_pipelined_rejects_simt():
+    import torch
+    import paper_2308_15152_b200 as emu
+    x = torch.zeros(4096, device="cuda")
+    with pytest.raises(emu.EmuError):
+        emu.emu_tcec_gemm_batched(8, 8, 8, 1.0, x, 8, 0, x, 8, 0, 0.0, x, 8, 64, 1, "fp16", None, 0, PIPE | SIMT)
+    with pytest.raises(emu.EmuError):   # no pipelined form of the map / scan users
+        emu.emu_tcec_givens_batched(8, 1, 2, 3, x, x, 8, 0, x, 8, 0, 1, "fp16", None, PIPE)

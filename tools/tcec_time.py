@@ -36,18 +36,21 @@ fl = 2.0 * batch * m ** 3
 for mode in ("fp16", "tf32"):
     ms = t_ms(lambda: emu.emu_sgemm_batched(m, m, m, 1.0, A, m, m * m, B, m, m * m, 0.0, C, m, m * m, batch, mode))
     out[f"c2_{mode}_library"] = round(fl / ms / 1e9, 1)
-    for flags, name in ((0, "tc"), (1, "tc_noec"), (2, "simt")):
+    for flags, name in ((0, "tc"), (1, "tc_noec"), (2, "simt"), (4, "pipelined"), (5, "pipelined_noec")):
         ms = t_ms(lambda: emu.emu_tcec_gemm_batched(m, m, m, 1.0, A, m, m * m, B, m, m * m, 0.0, C, m, m * m,
                                                     batch, mode, None, 0, flags), it=5 if flags & 2 else 20)
         out[f"c2_{mode}_tcec_{name}"] = round(fl / ms / 1e9, 1)
-# structured: batched Householder / Givens on 32 x 32 x 4096-column blocks, scan
-for hm in (32, 128):
+# structured: batched Householder / Givens on m x m reflectors times m x 128 blocks, scan
+for hm in (32, 128, 256):
     nb, n = 4096, 128
     V = torch.nn.functional.normalize(torch.rand(nb, hm, device="cuda") - 0.5, dim=1)
     X = torch.rand(nb, n, hm, device="cuda")
     Y = torch.empty_like(X)
     ms = t_ms(lambda: emu.emu_tcec_householder_batched(hm, n, V, hm, X, hm, n * hm, Y, hm, n * hm, nb, "fp16"))
     out[f"householder_m{hm}_fp16_TFs"] = round(2.0 * nb * hm * hm * n / ms / 1e9, 1)
+    ms = t_ms(lambda: emu.emu_tcec_householder_batched(hm, n, V, hm, X, hm, n * hm, Y, hm, n * hm, nb, "fp16",
+                                                       None, 4))
+    out[f"householder_m{hm}_fp16_pipelined_TFs"] = round(2.0 * nb * hm * hm * n / ms / 1e9, 1)
     CS = torch.rand(nb, 2, device="cuda")
     ms = t_ms(lambda: emu.emu_tcec_givens_batched(hm, n, 1, hm - 2, CS, X, hm, n * hm, Y, hm, n * hm, nb, "fp16"))
     out[f"givens_m{hm}_fp16_TFs"] = round(2.0 * nb * hm * hm * n / ms / 1e9, 1)
