@@ -374,6 +374,77 @@ static float tc_instr(orc_tc tc, int emin, float d, const float* a, const float*
     return d;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Exact sums of binary32 products (the "ideal" model's TF32 block sums):    */
+/* a fixed-point accumulator of XACC_LIMBS 32-bit digits (held in int64 for  */
+/* carry room) with unit 2^XACC_LSB, wide enough for any product of two      */
+/* binary32 values (2^-298 .. 2^256) and any block of up to 2^20 of them.     */
+/* ------------------------------------------------------------------------ */
+#define XACC_LSB (-320)
+#define XACC_LIMBS 20                    /* 640 bits: 2^-320 .. 2^320 */
+typedef struct { int64_t d[XACC_LIMBS]; } xacc;
+
+static void xacc_clear(xacc* a) { memset(a->d, 0, sizeof(a->d)); }
+
+static void xacc_add(xacc* a, xval v)   /* a += v exactly (|v.sig| < 2^48) */
+{
+    if (v.sig == 0) return;
+    int64_t sg = v.sig < 0 ? -1 : 1;
+    uint64_t m = (uint64_t)(v.sig < 0 ? -v.sig : v.sig);
+    int pos = v.ex - XACC_LSB;           /* bit position of m's lsb */
+    if (pos < 0) {                       /* below 2^-320: unreachable for TF32 products */
+        if (-pos >= 64) return;          /* (>= 2^-318); dropped bits only, never read */
+        m >>= -pos;
+        pos = 0;
+    }
+    while (m) {
+        int limb = pos >> 5, sh = pos & 31;
+        uint64_t part = (m << sh) & 0xffffffffull;
+        a->d[limb] += sg * (int64_t)part;
+        m = (sh == 0) ? (m >> 32) : (m >> (32 - sh));
+        pos = (limb + 1) << 5;
+    }
+}
+
+/* RN (ties to even) of the accumulated value to binary32, subnormals included */
+static float xacc_to_float_rn(const xacc* a)
+{
+    int64_t d[XACC_LIMBS];
+    memcpy(d, a->d, sizeof(d));
+    /* carry-normalise to digits in [0, 2^32) with the sign in the top carry */
+    int64_t carry = 0;
+    for (int i = 0; i < XACC_LIMBS; ++i) {
+        int64_t v = d[i] + carry;
+        carry = v >> 32;                 /* arithmetic shift: floor division */
+        d[i] = v - (carry << 32);
+    }
+    int neg = carry < 0;
+    if (neg) {                           /* magnitude of the two's complement value */
+        int64_t c = 1;
+        for (int i = 0; i < XACC_LIMBS; ++i) {
+            int64_t v = (0xffffffffll - d[i]) + c;
+            c = v >> 32;
+            d[i] = v & 0xffffffffll;
+        }
+    }
+    int top = -1;
+    for (int i = XACC_LIMBS - 1; i >= 0 && top < 0; --i)
+        if (d[i]) { int b = 31; while (!((d[i] >> b) & 1)) --b; top = i * 32 + b; }
+    if (top < 0) return 0.0f;
+    int e = top + XACC_LSB;              /* floor(log2 |value|) */
+    int q = (e >= -126 ? e - 23 : -149) - XACC_LSB;   /* quantum bit position */
+#define XBIT(p) ((p) < 0 ? 0 : (int)((d[(p) >> 5] >> ((p) & 31)) & 1))
+    uint64_t r = 0;
+    for (int p = top; p >= q && p >= 0; --p) r = (r << 1) | (uint64_t)XBIT(p);
+    if (q > top) r = 0;
+    int half = XBIT(q - 1), sticky = 0;
+    for (int p = q - 2; p >= 0 && !sticky; --p) sticky = XBIT(p);
+#undef XBIT
+    if (half && (sticky || (r & 1))) r += 1;
+    float v = ldexpf((float)r, q + XACC_LSB);   /* r <= 2^24: exact; overflow -> Inf */
+    return neg ? -v : v;
+}
+
 /*
  * The tensor-core model at instruction level, for comparison with the
  * standalone tcgen05 probe (probe/tc_probe.cu): n_instr chained MMA
@@ -472,10 +543,24 @@ static float emu_element(orc_tc tc, int mode, int corr_enable, int k, int kb,
             }
             d_hi = i128_to_float_rn(s1);
             d_corr = i128_to_float_rn(s2);
+        } else if (finite) {
+            /* TF32 parts: every product of two TF32 values is exact, but their
+               exponents span 2^-272 .. 2^256, so the block sum is formed exactly
+               in a fixed-point accumulator and rounded once to binary32 */
+            xacc s1, s2;
+            xacc_clear(&s1);
+            xacc_clear(&s2);
+            for (int p = p0; p < p1; ++p) {
+                xacc_add(&s1, xv_mul(ahi[p], bhi[p]));
+                if (corr_enable) {
+                    xacc_add(&s2, xv_mul(alo[p], bhi[p]));
+                    xacc_add(&s2, xv_mul(ahi[p], blo[p]));
+                }
+            }
+            d_hi = xacc_to_float_rn(&s1);
+            d_corr = xacc_to_float_rn(&s2);
         } else {
-            /* TF32 parts (products of 11-bit significands are exact in
-               binary64) or non-finite FP16 operands: binary64 ascending sum,
-               then one rounding to binary32 */
+            /* non-finite operands: IEEE propagation (Inf / NaN) in binary64 */
             double s1 = 0.0, s2 = 0.0;
             for (int p = p0; p < p1; ++p) {
                 s1 += (double)ahi[p] * (double)bhi[p];

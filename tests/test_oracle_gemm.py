@@ -211,3 +211,42 @@ def test_sgemm_f32_exact_and_bound():
     C = workloads.math_view(oracle.sgemm_f32(A, B, m, n, k)[0], m)[:4, :4].astype(np.float64)
     gamma = k * U / (1 - k * U)
     assert np.all(np.abs(C - exact) <= gamma * (np.abs(Am[:4]) @ np.abs(Bm[:, :4])))
+
+
+def _rn_f32(q):
+    """a Fraction rounded to the nearest binary32 (ties to even, subnormals, no
+    overflow handling needed here) -- written from the definition"""
+    from fractions import Fraction
+    if q == 0:
+        return 0.0
+    neg = q < 0
+    a = -q if neg else q
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    quantum = Fraction(2) ** (max(e, -126) - 23)
+    r, rem = divmod(a, quantum)
+    if rem > quantum / 2 or (rem == quantum / 2 and r % 2 == 1):
+        r += 1
+    v = float(r * quantum)
+    return -v if neg else v
+
+
+def test_tf32_ideal_block_sum_is_exact_across_exponents():
+    """the ideal model's TF32 block sums (R#9's reference model) are exact sums
+    rounded once: with terms 2^120, 2^-70, -2^120 a binary64 running sum would
+    lose 2^-70; exponent spreads of 2^+-100 vs Fractions"""
+    from fractions import Fraction
+    A = np.array([[2.0 ** 60], [1.0], [-(2.0 ** 60)]], dtype=np.float32)        # (k=3, m=1)
+    B = np.array([[2.0 ** 60, 2.0 ** -70, 2.0 ** 60]], dtype=np.float32)        # (n=1, k=3)
+    assert float(oracle.emu_gemm("tf32", A, B, 1, 1, 3)[0, 0, 0]) == 2.0 ** -70
+    rng = np.random.default_rng(77)
+    for trial in range(400):
+        k = int(rng.integers(1, 17))
+        sig = rng.integers(1024, 2048, size=(2, k)).astype(np.float64)
+        # wide spreads, and sums in binary32's subnormal range (products 2^-152 .. 2^-120)
+        e = rng.integers(-50, 51, size=(2, k)) if trial < 300 else rng.integers(-76, -59, size=(2, k))
+        v = (np.ldexp(sig, e - 10) * rng.choice([-1.0, 1.0], size=(2, k))).astype(np.float32)  # TF32-exact
+        got = float(oracle.emu_gemm("tf32", v[0].reshape(k, 1), v[1].reshape(1, k), 1, 1, k, kb=64)[0, 0, 0])
+        exact = sum((Fraction(float(x)) * Fraction(float(y)) for x, y in zip(v[0], v[1])), Fraction(0))
+        assert got == _rn_f32(exact), (trial, got, float(exact))
