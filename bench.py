@@ -408,6 +408,7 @@ def measure(args, cfg_name, mode, rank, world, local, steps, warmup, e2e=True, c
     for _ in range(max(3, warmup)):
         step()
     torch.cuda.synchronize()
+    kname = emu.emu_last_kernel_name()     # what the library dispatched for this workload
     # c1 is launch-latency bound (16 x 64^3): each step is one replay of a CUDA graph
     # holding the launch, so the host launch path is not what is timed
     graph = None
@@ -497,7 +498,6 @@ def measure(args, cfg_name, mode, rank, world, local, steps, warmup, e2e=True, c
     # cuBLAS measurement): its roofline uses the sustained peak; the burst fraction is
     # reported beside it
     tc_peak_sus = peaks["bf16_tflops_sustained"] * (1.0 if mode == "fp16" else 0.5)
-    kname = emu.emu_last_kernel_name()     # what the library dispatched for this workload
     kernel_ms = ms_per_step / max(1, launches / steps)    # per launch of the dominant kernel
     if cfg_name in ("c1", "c2", "c5"):
         bytes_launch = 4.0 * (m * k + k * n + m * n) * batch

@@ -1,8 +1,8 @@
 """Copy one round's ncu evidence into profiles/: the raw-metric summaries of the
-full captures (profiles/r01_ncu_final.json), the DRAM traffic per launch that
+full captures (profiles/rNN_ncu_final.json), the DRAM traffic per launch that
 bench.py reports as roofline.traffic (profiles/traffic.json) and the launch list.
 
-  python tools/update_profiles.py TAG     (reads gpurun_out/prof_*_TAG.ncu-rep)
+  python tools/update_profiles.py TAG [ROUND]   (reads gpurun_out/prof_*_TAG.ncu-rep; ROUND e.g. r02)
 """
 import json
 import os
@@ -23,6 +23,7 @@ def val(s):
 
 def main():
     tag = sys.argv[1]
+    rnd = sys.argv[2] if len(sys.argv) > 2 else "r02"
     out = os.path.join(ROOT, "gpurun_out")
     reps = {}
     for c in ("c2_fp16", "c2_tf32", "c3_fp16"):
@@ -37,12 +38,12 @@ def main():
         rd, wr = val(d["dram__bytes_read.sum"]), val(d["dram__bytes_write.sum"])
         traffic[c] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                       "kernel": d["Kernel Name"], "ncu_duration": d["gpu__time_duration.sum"],
-                      "source": f"ncu --set full --clock-control none, one launch (round 1, {tag})"}
-    json.dump(summ, open(os.path.join(ROOT, "profiles", "r01_ncu_final.json"), "w"), indent=1)
+                      "source": f"ncu --set full --clock-control none, one launch ({rnd}, {tag})"}
+    json.dump(summ, open(os.path.join(ROOT, "profiles", f"{rnd}_ncu_final.json"), "w"), indent=1)
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
     lst = os.path.join(out, f"launches_c2_fp16_{tag}.csv")
     if os.path.exists(lst):
-        shutil.copy(lst, os.path.join(ROOT, "profiles", "r01_launches_c2_fp16.csv"))
+        shutil.copy(lst, os.path.join(ROOT, "profiles", f"{rnd}_launches_c2_fp16.csv"))
     print(json.dumps(traffic, indent=1))
 
 
