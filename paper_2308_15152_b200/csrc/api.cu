@@ -423,7 +423,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     using Cfg = emu::PairTsCfg<MODE, BN, SPLITC, ASTAT, LONGK>;
     {
         // the dynamic shared-memory attribute, once per device and instantiation
-        static bool attr_set[64] = {};
+        static bool attr_set[kMaxDevices] = {};
         std::lock_guard<std::mutex> lk(g_dev_mu);
         if (!attr_set[dev]) {
             if (cudaFuncSetAttribute(emu::emu_sgemm_pair_ts_kernel<MODE, RANGE, BN, SPLITC, ASTAT, TA, TB, false, LONGK, Ops>,

@@ -751,17 +751,19 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 if (Ops::custom_store) {
                     const int r = mrow0 + (int)(q * 32 + lane);
                     const int col0 = nt * Cfg::BN + (int)(h * HALF);
-                    if (r < p.m) ops.store(b, r, col0, creg, min(HALF, p.n - col0));
+                    if (r < p.m && col0 < p.n) ops.store(b, r, col0, creg, min(HALF, p.n - col0));
                 } else if (p.tma_store) {
                     // each warp stages and TMA-stores its own 32 rows x HALF columns (no
                     // CTA-wide barrier: a warp moves on to the next tile's drains at once)
                     float* dst = cstage + e * (32 * HALF);
                     if (lane == 0) ptx::bulk_wait_group_read0();   // this warp's previous store read its block
                     __syncwarp();
+                    if (lane == 0) TRACE_AT(3 + e, 16, j);
 #pragma unroll
                     for (int jj = 0; jj < HALF; ++jj) dst[jj * 32 + lane] = fmaf(p.alpha, creg[jj], 0.0f);
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
+                    if (lane == 0) TRACE_AT(3 + e, 17, j);
                     if (lane == 0) {   // box: 32 rows x HALF columns
                         ptx::tma_store_3d(&tmC, dst, mrow0 + (int)(q * 32), nt * Cfg::BN + (int)(h * HALF), b);
                         ptx::bulk_commit_group();

@@ -19,7 +19,8 @@ import prof_roles  # noqa: E402
 
 NAMES = {1: "prod_issue", 2: "spl_got_f32", 3: "spl_got_op", 4: "spl_done", 5: "mma_corr_start",
          6: "mma_corr_commit", 7: "mma_hi_start", 8: "mma_hi_commit", 9: "mma_got_op", 10: "epi_corr_full",
-         11: "epi_corr_rel", 12: "epi_hi_full", 13: "epi_hi_rel", 14: "epi_store_start", 15: "epi_store_end"}
+         11: "epi_corr_rel", 12: "epi_hi_full", 13: "epi_hi_rel", 14: "epi_store_start", 15: "epi_store_end",
+         16: "epi_store_waited", 17: "epi_store_staged"}
 
 
 def main():
@@ -109,6 +110,9 @@ def main():
     pair_stats(8, 12, "hi commit -> combine sees hi_full")
     pair_stats(12, 13, "combine: hi ld + release")
     pair_stats(14, 15, "epilogue store")
+    pair_stats(14, 16, "  store: wait previous bulk read")
+    pair_stats(16, 17, "  store: stage 32 x 32 in smem + fence")
+    pair_stats(17, 15, "  store: issue TMA store")
     pair_stats(3, 2, "splitter: got op slot -> got f32")
     pair_stats(2, 4, "splitter: split work")
     x4, x2 = np.array(seq[4]), np.array(seq[3])
