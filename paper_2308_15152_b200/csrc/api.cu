@@ -494,6 +494,8 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
         // power under the power cap (profiles/r01_summary.md); A-stationary units read A
         // and B once: default policy
         p.l2_policy = pol >= 0 ? pol : (ASTAT ? 0 : 3);
+        static const int c_ef = env_int("EMU_C_EVICT_FIRST", 0, 0, 1);   // tuning only
+        if (c_ef) p.l2_policy |= 4;
     }
     p.range_flag = MODE == 0 ? range_flag : nullptr;
     p.row_max = row_max;

@@ -765,7 +765,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     __syncwarp();
                     if (lane == 0) TRACE_AT(3 + e, 17, j);
                     if (lane == 0) {   // box: 32 rows x HALF columns
-                        ptx::tma_store_3d(&tmC, dst, mrow0 + (int)(q * 32), nt * Cfg::BN + (int)(h * HALF), b);
+                        if (p.l2_policy & 4)   // C stores evict_first (tuning, EMU_C_EVICT_FIRST)
+                            ptx::tma_store_3d_hint(&tmC, dst, mrow0 + (int)(q * 32), nt * Cfg::BN + (int)(h * HALF), b,
+                                                   ptx::l2_policy_evict_first());
+                        else
+                            ptx::tma_store_3d(&tmC, dst, mrow0 + (int)(q * 32), nt * Cfg::BN + (int)(h * HALF), b);
                         ptx::bulk_commit_group();
                     }
                 } else {
