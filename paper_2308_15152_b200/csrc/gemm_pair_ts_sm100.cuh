@@ -752,6 +752,21 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     const int r = mrow0 + (int)(q * 32 + lane);
                     const int col0 = nt * Cfg::BN + (int)(h * HALF);
                     if (r < p.m && col0 < p.n) ops.store(b, r, col0, creg, min(HALF, p.n - col0));
+                } else if (p.tma_store && (p.l2_policy & 8)) {
+                    // (TF32 default, EMU_C_BOX128) the 4 warps of a column group stage their 32-row
+                    // blocks into one 128-row x HALF box, stored by one TMA store (512-byte
+                    // column segments in global memory instead of 128-byte ones)
+                    float* dstg = cstage + h * (128 * HALF);
+                    if (q == 0 && lane == 0) ptx::bulk_wait_group_read0();   // the group's previous store
+                    ptx::named_bar_sync(1 + h, 128);
+#pragma unroll
+                    for (int jj = 0; jj < HALF; ++jj) dstg[jj * 128 + q * 32 + lane] = fmaf(p.alpha, creg[jj], 0.0f);
+                    ptx::fence_proxy_async_smem();
+                    ptx::named_bar_sync(1 + h, 128);
+                    if (q == 0 && lane == 0) {
+                        ptx::tma_store_3d(&tmC, dstg, mrow0, nt * Cfg::BN + (int)(h * HALF), b);
+                        ptx::bulk_commit_group();
+                    }
                 } else if (p.tma_store) {
                     // each warp stages and TMA-stores its own 32 rows x HALF columns (no
                     // CTA-wide barrier: a warp moves on to the next tile's drains at once)
