@@ -250,3 +250,15 @@ def test_tf32_ideal_block_sum_is_exact_across_exponents():
         got = float(oracle.emu_gemm("tf32", v[0].reshape(k, 1), v[1].reshape(1, k), 1, 1, k, kb=64)[0, 0, 0])
         exact = sum((Fraction(float(x)) * Fraction(float(y)) for x, y in zip(v[0], v[1])), Fraction(0))
         assert got == _rn_f32(exact), (trial, got, float(exact))
+
+
+def test_entry_references_equal_full_references():
+    """O4 / O5 at sampled entries (the full-size accuracy gates) are the same
+    loops as the full references: equal at every sampled entry, batched, ragged"""
+    A, B = workloads.make_operands(3, 37, 29, 53, seed=5)
+    g = np.random.default_rng(6)
+    b, i, j = g.integers(0, 3, 200), g.integers(0, 37, 200), g.integers(0, 29, 200)
+    R = oracle.gemm_f64(A, B, 37, 29, 53)
+    S = oracle.sgemm_f32(A, B, 37, 29, 53)
+    assert np.array_equal(oracle.gemm_f64_entries(A, B, 37, 29, 53, b, i, j), R[b, j, i])
+    assert np.array_equal(oracle.sgemm_f32_entries(A, B, 37, 29, 53, b, i, j), S[b, j, i])
