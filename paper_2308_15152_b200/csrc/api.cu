@@ -490,16 +490,27 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     p.corr = (flags & EMU_FLAG_NO_CORRECTION) ? 0 : 1;
     p.tma_store = tma_store;
     p.prefetch = prefetch_distance();
+    // long-k streaming tiles: one cluster per tile; the running (persistent) clusters take over
+    // the rest by cluster launch control, in launch order, each claiming its next tile p.clc
+    // k-stages before its current one's loads end (EMU_TS_CLC; 0: static order, cluster c
+    // takes tiles c, c + 74, ...).  The clusters that share an operand panel then start it
+    // close together instead of drifting apart over the launch, so the panel is reused in L2:
+    // c3 DRAM reads 70 -> 37 GB per launch (profiles/r02_summary.md)
+    static const int clc_env = env_int("EMU_TS_CLC", 8, 0, 1 << 20);   // tuning only
+    p.clc = LONGK && p.num_tiles <= (1LL << 30) ? clc_env : 0;   // LONGK: units = tiles
     {
-        static const int gm = env_int("EMU_GROUP_M", 2, 1, 1 << 20);    // tuning only (c3 DRAM bytes: 2 < 4 < 8 < 16, profiles/r01_summary.md)
-        static const int pol = env_int("EMU_L2_POLICY", -1, -1, 3);    // tuning only (-1: default below)
-        p.group_m = gm;
-        // streaming tiles (grouped raster): B evict_first (each B tile is used by the two
-        // row blocks of a group at about the same time, then not again), A evict_last (a
+        // raster group: m-tiles per group walking the n-tiles together (EMU_GROUP_M, tuning);
+        // dynamic order: 3 (each B panel is read by 3 row blocks close together)
+        static const int gm = env_int("EMU_GROUP_M", 0, 0, 1 << 20);
+        static const int pol = env_int("EMU_L2_POLICY", -1, -1, 31);   // tuning only (-1: default below)
+        p.group_m = gm ? gm : (p.clc ? 3 : 2);
+        // streaming tiles (grouped raster), static order: B evict_first (each B tile is used by the
+        // two row blocks of a group at about the same time, then not again), A evict_last (a
         // group's rows are reread by every n-tile): c3 fp16 +5 %, tf32 +3.5 % from lower DRAM
-        // power under the power cap (profiles/r01_summary.md); A-stationary units read A
-        // and B once: default policy
-        p.l2_policy = pol >= 0 ? pol : (ASTAT ? 0 : 3);
+        // power under the power cap (profiles/r01_summary.md).  Dynamic order: B normal (the
+        // group's readers come within ~10 us of each other), A evict_last.  A-stationary units
+        // read A and B once: default policy.  Bit 4 (tuning): B evict_last.
+        p.l2_policy = pol >= 0 ? pol : (ASTAT ? 0 : (p.clc ? 2 : 3));
         if (c_box128) p.l2_policy |= 8;
         static const int c_ef = env_int("EMU_C_EVICT_FIRST", 0, 0, 1);   // tuning only
         if (c_ef) p.l2_policy |= 4;
@@ -514,7 +525,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     p.num_units = ASTAT ? (long long)p.tiles_m * batch : p.num_tiles;
     p.unit_tiles = ASTAT ? p.tiles_n : 1;
     if (ASTAT && p.num_k_stages > Cfg::ASLOTS) return EMU_STATUS_NOT_SUPPORTED;   // dispatch guarantees it
-    const long long clusters = std::min<long long>(p.num_units, sms / 2);
+    const long long clusters = p.clc ? p.num_units : std::min<long long>(p.num_units, sms / 2);
     // the multicast epilogue is its own instantiation (MC): the plain kernels carry no
     // per-destination loop
     bool launched = false;

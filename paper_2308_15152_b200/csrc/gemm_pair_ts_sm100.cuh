@@ -79,7 +79,11 @@ struct PairTsCfg {
     static constexpr int S32 = S32_FIT < S32_MAX ? S32_FIT : S32_MAX;
     static constexpr uint32_t KCOLS = 8;                       // TMEM columns per MMA K step
     static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
-    static constexpr uint32_t BAR_BYTES = 8 * (2 * S32 + 2 * SOP + 4 + ASLOTS) + 16;
+    // CLC (long-k streaming tiles, p.clc): two 16-byte cluster-launch-control responses
+    // and their full / empty barriers precede the other barriers
+    static constexpr uint32_t CLC_BYTES = LONGK ? 32 + 8 * 6 : 0;
+    static constexpr int CLC_CONSUMERS = 2 * 1 + 1 + 2 * 8 + 2 * 16;   // producer x2, MMA, splitter, combine warps
+    static constexpr uint32_t BAR_BYTES = CLC_BYTES + 8 * (2 * S32 + 2 * SOP + 4 + ASLOTS) + 16;
     static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + CSTAGE_BYTES + BAR_BYTES;
     // warpgroup 0: producer, MMA issuer, 2 idle; warpgroups 1-2: 8 splitter warps
     // (2 per TMEM lane quadrant, 16 k each); warpgroups 3-6: 16 combine warps (4 per
@@ -151,7 +155,12 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     uint8_t* f32buf = smem;
     uint8_t* opbuf = smem + Cfg::S32 * Cfg::F32_STAGE;
     float* cstage = reinterpret_cast<float*>(opbuf + Cfg::SOP * Cfg::OP_STAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(opbuf + Cfg::SOP * Cfg::OP_STAGE + Cfg::CSTAGE_BYTES);
+    uint8_t* barbase = opbuf + Cfg::SOP * Cfg::OP_STAGE + Cfg::CSTAGE_BYTES;   // 1024-byte aligned
+    uint4* clc_resp = reinterpret_cast<uint4*>(barbase);                       // [2] (CLC_BYTES)
+    uint64_t* clc_full = reinterpret_cast<uint64_t*>(barbase + 32);           // [2]
+    uint64_t* clc_empty = clc_full + 2;                                        // [2] (leader's used)
+    uint64_t* clc_req = clc_empty + 2;                                         // [1] (leader): claim now
+    uint64_t* bars = reinterpret_cast<uint64_t*>(barbase + Cfg::CLC_BYTES);
     uint64_t* f32_full = bars;
     uint64_t* f32_empty = f32_full + Cfg::S32;
     uint64_t* op_full = f32_empty + Cfg::S32;
@@ -167,6 +176,20 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const long long num_units = p.num_units;
     const int R = ASTAT ? p.unit_tiles : 1;
+    // tile order: static (cluster c takes units c, c + ncl, ...) or, with CLC, the unit of
+    // each cluster launch this cluster cancels (in launch order: the clusters that share an
+    // operand panel start it close together, so it is reused in L2)
+    const bool clc = Cfg::LONGK && p.clc != 0;
+    auto clc_next = [&](uint32_t& ci, bool arrive) -> long long {
+        const uint32_t slot = ci & 1u, ph = (ci >> 1) & 1u;
+        ++ci;
+        ptx::mbar_wait(&clc_full[slot], ph);
+        const int x = ptx::clc_first_ctaid_x(&clc_resp[slot]);
+        ptx::fence_proxy_async_smem();   // our read before the next async-proxy write of the slot
+        __syncwarp(__activemask());
+        if (arrive) ptx::mbar_arrive_cluster(ptx::mapa_shared(&clc_empty[slot], 0));
+        return x < 0 ? -1 : (long long)(x >> 1);
+    };
     PROF_DECL
     TRACE_DECL
 #ifdef EMU_PROF
@@ -187,6 +210,13 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             ptx::mbar_init(&acc_empty[i], 2 * Cfg::NUM_EPI_WARPS);
         }
         for (int i = 0; i < Cfg::ASLOTS; ++i) ptx::mbar_init(&aslot_empty[i], 1);
+        if (Cfg::LONGK) {
+            for (int i = 0; i < 2; ++i) {
+                ptx::mbar_init(&clc_full[i], 1);
+                ptx::mbar_init(&clc_empty[i], Cfg::CLC_CONSUMERS);
+            }
+            ptx::mbar_init(clc_req, 1);
+        }
         ptx::fence_mbar_init();
         if (!Ops::gen_a) ptx::prefetch_tmap(&tmA);
         if (!Ops::gen_b) ptx::prefetch_tmap(&tmB);
@@ -208,14 +238,17 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             if (ptx::elect_one()) {
                 uint32_t s = 0, ph = 0;
                 // L2 hints (tuning, EMU_L2_POLICY): bit 0 -> B evict_first, bit 1 -> A evict_last
-                const uint64_t pol_a = ptx::l2_policy_evict_last(), pol_b = ptx::l2_policy_evict_first();
+                // bit 4 (tuning): B evict_last instead of evict_first
+                const uint64_t pol_a = ptx::l2_policy_evict_last(),
+                               pol_b = (p.l2_policy & 16) ? ptx::l2_policy_evict_last() : ptx::l2_policy_evict_first();
                 auto load = [&](uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, bool hint,
                                 uint64_t pol) {
                     if (hint) ptx::tma_load_3d(dst, map, bar, c0, c1, c2, pol);
                     else ptx::tma_load_3d_nohint(dst, map, bar, c0, c1, c2);
                 };
-                const bool hint_a = (p.l2_policy & 2) != 0, hint_b = (p.l2_policy & 1) != 0;
-                for (long long u = cid; u < num_units; u += ncl) {
+                const bool hint_a = (p.l2_policy & 2) != 0, hint_b = (p.l2_policy & 17) != 0;
+                uint32_t ci = 0;
+                for (long long u = cid; u >= 0 && u < num_units; u = clc ? clc_next(ci, true) : u + ncl) {
                     for (int j = 0; j < R; ++j) {
                         int b, mt, nt;
                         ts_unit_tile<ASTAT>(p, u, j, b, mt, nt);
@@ -225,6 +258,9 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                             PROF_T0();
                             ptx::mbar_wait_sleep(&f32_empty[s], ph ^ 1);
                             PROF_ADD(P_PROD_WAIT_EMPTY);
+                            // CLC: the next unit is claimed p.clc stages before this one's loads end,
+                            // so the clusters that share an operand panel start it close together
+                            if (clc && rank == 0 && j == R - 1 && ks == max(nks - p.clc, 0)) ptx::mbar_arrive(clc_req);
                             uint8_t* dst = f32buf + s * Cfg::F32_STAGE;
                             TRACE_AT(0, 1, ks);
                             // generated operands (Ops::gen_a / gen_b) are not loaded: the splitter
@@ -261,7 +297,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                 if constexpr (Cfg::SPLITC) {
                     // per k-block: P2 + P3 into D_corr (barrier pair 1), then P1 into D_hi (pair 0)
                     const uint32_t d_hi = tmem_base, d_corr = tmem_base + Cfg::BN;
-                    for (long long u = cid; u < num_units; u += ncl) {
+                    uint32_t ci = 0;
+                    for (long long u = cid; u >= 0 && u < num_units; u = clc ? clc_next(ci, true) : u + ncl) {
                         for (int j = 0; j < R; ++j) {
                             const bool lastA = ASTAT && j == R - 1;   // release the A slots after this tile
                             for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
@@ -376,7 +413,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                         }
                     }
                 } else {
-                    for (long long u = cid; u < num_units; u += ncl) {
+                    uint32_t ci = 0;
+                    for (long long u = cid; u >= 0 && u < num_units; u = clc ? clc_next(ci, true) : u + ncl) {
                         for (int kb = 0; kb < nkb; ++kb, ++acc_it) {
                             const int ks0 = kb * p.kb_stages;
                             const int ks1 = min(ks0 + p.kb_stages, nks);
@@ -428,6 +466,22 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     }
                 }
             }
+        } else if (warp == 3) {
+            // -------------------------------------------- CLC scheduler (leader CTA): keeps the
+            // next unit's response one ahead of the roles that consume it
+            if (clc && rank == 0 && ptx::elect_one()) {
+                const uint32_t peer_full = ptx::mapa_shared(&clc_full[0], 1);
+                for (uint32_t i = 0;; ++i) {
+                    const uint32_t slot = i & 1u, ph = (i >> 1) & 1u;
+                    ptx::mbar_wait_sleep(clc_req, i & 1u);   // the producer nears the end of its unit
+                    ptx::mbar_wait(&clc_empty[slot], ph ^ 1u);
+                    ptx::mbar_arrive_expect_tx(&clc_full[slot], 16);
+                    ptx::mbar_arrive_expect_tx_cluster(peer_full + 8 * slot, 16);
+                    ptx::clc_try_cancel(&clc_resp[slot], &clc_full[slot]);
+                    ptx::mbar_wait(&clc_full[slot], ph);
+                    if (ptx::clc_first_ctaid_x(&clc_resp[slot]) < 0) break;
+                }
+            }
         }
     } else if (warp < Cfg::EPI_WARP0) {
         // ------------------------------------------------ splitters (256 threads)
@@ -442,7 +496,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0, unit_it = 0;
         uint32_t nonfinite = 0;
         const bool chk = (RANGE & 1) && p.range_flag != nullptr;   // the FP16 overflow flag was asked for
-        for (long long u = cid; u < num_units; u += ncl, ++unit_it) {
+        uint32_t ci = 0;
+        for (long long u = cid; u >= 0 && u < num_units; u = clc ? clc_next(ci, lane == 0) : u + ncl, ++unit_it) {
             for (int j = 0; j < R; ++j) {
                 const bool doA = !ASTAT || j == 0;
                 // generated operands: this thread's problem, row of A and column of B
@@ -613,8 +668,8 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t h = e >> 2;                     // column group: tile columns [HALF h, +HALF)
         const float scale = MODE == 0 ? (1.0f / 2048.0f) : 1.0f;
         const uint32_t acc_empty_leader = ptx::mapa_shared(&acc_empty[0], 0);   // + 8 * buffer
-        uint32_t acc_it = 0;
-        for (long long u = cid; u < num_units; u += ncl) {
+        uint32_t acc_it = 0, ci = 0;
+        for (long long u = cid; u >= 0 && u < num_units; u = clc ? clc_next(ci, lane == 0) : u + ncl) {
             for (int j = 0; j < R; ++j) {
                 int b, mt, nt;
                 ts_unit_tile<ASTAT>(p, u, j, b, mt, nt);

@@ -103,6 +103,8 @@ struct GemmParams {
     long long num_tiles;
     long long num_units;          // TS kernel: work units (A-stationary: one (batch, m-pair) row block each)
     int unit_tiles;               // TS kernel: tiles per unit (A-stationary: tiles_n, else 1)
+    int clc;                      // TS kernel (long-k rings): dynamic tile order by cluster launch
+                                  // control -- the grid has one cluster per unit
     int num_k_stages;             // ceil(k / 32)
     int kb_stages;                // KB / 32
     int corr;                     // 1 = the paper's method; 0 = "correction off" control

@@ -201,6 +201,38 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr)
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// arrive + expect_tx on an mbarrier given by its shared::cluster address (the peer's)
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;"
+                 ::"r"(cluster_addr), "r"(bytes) : "memory");
+}
+
+// ------------------------------------------------------- cluster launch control
+// Dynamic persistent scheduling: cancel the launch of a not-yet-running cluster of this
+// grid and take over its work.  The 16-byte response is written to `resp` in every CTA
+// of the cluster (same shared-memory offset) with a complete_tx of 16 bytes on `bar`
+// there.
+__device__ __forceinline__ void clc_try_cancel(void* resp, uint64_t* bar)
+{
+    asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes"
+                 ".multicast::cluster::all.b128 [%0], [%1];"
+                 ::"r"(smem_u32(resp)), "r"(smem_u32(bar)) : "memory");
+}
+
+// decode a response: the canceled cluster's first CTA x index, or -1 if none was canceled
+__device__ __forceinline__ int clc_first_ctaid_x(const void* resp)
+{
+    uint32_t x = 0, valid = 0;
+    asm volatile("{\n\t.reg .pred p1;\n\t.reg .b128 r;\n\t"
+                 "ld.shared.b128 r, [%2];\n\t"
+                 "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p1, r;\n\t"
+                 "selp.u32 %1, 1, 0, p1;\n\t"
+                 "@p1 clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%0, _, _, _}, r;\n\t}"
+                 : "=r"(x), "=r"(valid) : "r"(smem_u32(resp)) : "memory");
+    return valid ? (int)x : -1;
+}
+
 // wait whose arrivals may come from the peer CTA (release.cluster on their side)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity)
 {

@@ -37,8 +37,10 @@ def main():
     L = ctypes.CDLL(LIB)
     if cfg == "c2":
         batch, m, n, k = 1024, 256, 256, 256
-    else:
+    elif cfg == "c3h":
         batch, m, n, k = 1, 8192, 8192, 8192
+    else:
+        batch, m, n, k = 1, 16384, 16384, 16384
     A = torch.rand(batch, k, m, device="cuda") * 2 - 1
     Bm = torch.rand(batch, n, k, device="cuda") * 2 - 1
     C = torch.empty(batch, n, m, device="cuda")
@@ -69,7 +71,7 @@ def main():
     kern = os.environ.get("EMU_KERNEL", "ts")
     nspl = 8 if kern in ("single", "ts") or m <= 128 else 16
     nepi = 16 if kern == "ts" and m > 128 else 8
-    ctas_mma = ctas if nspl == 8 else ctas // 2     # pair kernels: the MMA issuer lives in the leader CTA
+    ctas_mma = ctas if (kern == "single" or m <= 128) else ctas // 2   # pair kernels: the MMA issuer lives in the leader CTA
     per = {"prod_wait_empty": 1, "mma_wait_acc": ctas_mma / ctas, "mma_wait_op": ctas_mma / ctas,
            "mma_issue": ctas_mma / ctas, "spl_wait_f32": nspl, "spl_wait_op": nspl, "spl_work": nspl,
            "epi_wait_acc": nepi, "epi_drain": nepi, "epi_store": nepi}

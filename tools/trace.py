@@ -2,7 +2,7 @@
 runs one c2 launch and prints the per-k-block timeline statistics of the TS
 kernel -- where the MMA issuer, the splitters and the combine warps wait.
 
-  python tools/trace.py [fp16|tf32] [batch]
+  python tools/trace.py [fp16|tf32] [batch | c3 | c3h]   (c3: one 16384^3 GEMM, c3h: 8192^3)
 """
 import ctypes
 import os
@@ -25,11 +25,15 @@ NAMES = {1: "prod_issue", 2: "spl_got_f32", 3: "spl_got_op", 4: "spl_done", 5: "
 
 def main():
     mode = 0 if (len(sys.argv) <= 1 or sys.argv[1] == "fp16") else 1
-    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+    shape = sys.argv[2] if len(sys.argv) > 2 else "1024"
+    if shape in ("c3", "c3h"):
+        batch, m = 1, (16384 if shape == "c3" else 8192)
+    else:
+        batch, m = int(shape), 256
     os.environ["EMU_EXTRA_DEFS"] = (os.environ.get("EMU_EXTRA_DEFS", "") + " -DEMU_TRACE").strip()
     prof_roles.build()
     L = ctypes.CDLL(prof_roles.LIB)
-    m = n = k = 256
+    n = k = m
     A = torch.rand(batch, k, m, device="cuda") * 2 - 1
     B = torch.rand(batch, n, k, device="cuda") * 2 - 1
     C = torch.empty(batch, n, m, device="cuda")
