@@ -464,7 +464,8 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     if (g_mdst && g_mdst->n > 1) tma_store = 0;   // multicast: st.global to every destination
     if (Cfg::CSTAGE_BYTES == 0) tma_store = 0;     // long-k variant: no C staging area
     if (Ops::custom_store) tma_store = 0;          // the user's epilogue stores
-    static const int tma_store_env = env_int("EMU_TMA_STORE", 1, 0, 1);   // tuning only (0: st.global)
+    // tuning only (0: st.global from the combine warps; c2 fp16 204.7 vs 236.2 TF, ABBA)
+    static const int tma_store_env = env_int("EMU_TMA_STORE", 1, 0, 1);
     if (!tma_store_env) tma_store = 0;
     if (tma_store) {
         const uint64_t sC = c_b ? (uint64_t)strideC : (((uint64_t)ldc * (uint64_t)n + 3) & ~uint64_t(3));
@@ -563,7 +564,7 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
 // device-API entries): tile width, split commit, A-stationary, long-k rings
 struct TsPlan {
     int n;
-    bool sc, as, lk, aslk;
+    bool sc, as, lk;
 };
 
 TsPlan ts_plan(int mode, int m, int n, int k, int batch, int sms, bool multicast)
@@ -586,10 +587,6 @@ TsPlan ts_plan(int mode, int m, int n, int k, int batch, int sms, bool multicast
     // long k, streaming tiles: deeper operand / FP32 rings instead of the C staging area
     static const int ts_lk_env = env_int("EMU_TS_LONGK", 1, 0, 1);   // tuning only (default on)
     t.lk = t.sc && !t.as && ts_lk_env && (k + 31) / 32 >= 64;
-    // A-stationary with the long-k rings (no C staging: st.global epilogue, 8 operand slots,
-    // 6 FP32 stages; tuning, EMU_TS_ASTAT_LK=1)
-    static const int ts_aslk_env = env_int("EMU_TS_ASTAT_LK", 0, 0, 1);
-    t.aslk = t.as && ts_aslk_env && mode == EMU_SPLIT_FP16;
     return t;
 }
 
@@ -612,20 +609,6 @@ emu_status run_pipelined(int dev, int sms, int m, int n, int k, float alpha, con
     if (t.n == 64) EMU_RUN_P(64, false, false, false);
     EMU_RUN_P(128, false, false, false);
 #undef EMU_RUN_P
-}
-
-// A-stationary with the long-k rings (tuning, EMU_TS_ASTAT_LK): plain FP16 only
-template <int MODE, int RANGE>
-emu_status run_ts_astat_lk(int dev, int sms, int m, int n, int k, float alpha, const float* A, int lda,
-                           long long strideA, const float* B, int ldb, long long strideB, float beta, float* C, int ldc,
-                           long long strideC, int batch, cudaStream_t s, int kblock, unsigned flags)
-{
-    if constexpr (MODE == 0 && RANGE == 0) {
-        return run_gemm_pair_ts<0, 0, 128, true, true, false, false, true>(
-            dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC, batch, s, nullptr,
-            kblock, flags, nullptr, nullptr);
-    }
-    return EMU_STATUS_NOT_SUPPORTED;
 }
 
 }  // namespace
@@ -760,12 +743,9 @@ static emu_status gemm_impl(int m, int n, int k, float alpha, const float* A, in
     // (EMU_TS_SPLITC=0) stay selectable for comparison.
     const TsPlan plan = ts_plan(mode, m, n, k, batch, sms, g_mdst != nullptr);
     const int ts_n = plan.n;
-    const bool ts_sc = plan.sc, ts_as = plan.as, ts_lk = plan.lk, ts_aslk = plan.aslk;
+    const bool ts_sc = plan.sc, ts_as = plan.as, ts_lk = plan.lk;
 #define EMU_RUN_TS(MODE_, RANGE_)                                                                                      \
     do {                                                                                                               \
-        if (ts_aslk && (rs = run_ts_astat_lk<MODE_, RANGE_>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb,         \
-                                                        strideB, beta, C, ldc, strideC, batch, s, kblock, flags))      \
-                           != EMU_STATUS_NOT_SUPPORTED) break;                                                         \
         if (ts_as)                                                                                                     \
             { rs = run_gemm_pair_ts<MODE_, RANGE_, 128, true, true>(dev, sms, m, n, k, alpha, A, lda, strideA, B, ldb, \
                                                                     strideB, beta, C, ldc, strideC, batch, s,          \

@@ -43,7 +43,7 @@ namespace emu {
 // FP16 8 operand slots (a whole KB = 128 k-block plus half of the next) and 6 FP32 stages
 template <int MODE, int BN_ = 128, bool SPLITC_ = true, bool ASTAT_ = false, bool LONGK_ = false>
 struct PairTsCfg {
-    static constexpr bool LONGK = LONGK_;   // with ASTAT_ (tuning): A-stationary without C staging
+    static constexpr bool LONGK = LONGK_ && !ASTAT_;
     static constexpr int BM = 128;                      // A rows per CTA (pair M = 256)
     static constexpr int BN = BN_;                      // pair tile N = D columns per CTA
     static constexpr int BNC = BN / 2;                  // B columns staged per CTA
