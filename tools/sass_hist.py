@@ -1,7 +1,7 @@
 """SASS opcode histogram of the built libraries (CPU; cuobjdump): per kernel,
 the instructions that prove the Blackwell path -- tcgen05 MMAs (UTCHMMA /
 UTCQMMA, .2CTA = cta_group::2), TMEM loads/stores (LDTM / STTM), TMA
-(UTMALDG / UTMASTG / UTMAPF), the packed FP32 math of the combine (FFMA2 /
+(UTMALDG / UTMASTG / UTMAPF), cluster launch control (UGETNEXTWORKID = try_cancel), the packed FP32 math of the combine (FFMA2 /
 FADD2 / FMUL2) and the split's conversions (F2FP).  Writes
 profiles/r02_sass_hist.json.
 
@@ -17,7 +17,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIBS = ["paper_2308_15152_b200/libemusgemm.so", "probe/libtcprobe.so"]
 KEYS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UTMALDG", "UTMASTG", "UTMAPF", "FFMA2", "FADD2",
-        "FMUL2", "F2FP", "HFMA2", "LDS", "STS", "LDG", "STG", "SYNCS", "ELECT", "BAR", "MEMBAR"]
+        "FMUL2", "F2FP", "HFMA2", "LDS", "STS", "LDG", "STG", "SYNCS", "ELECT", "BAR", "MEMBAR", "UGETNEXTWORKID"]
 
 
 def main():
