@@ -19,7 +19,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # 9 m-pairs x 11 n-tiles = 99 tiles (> 74 clusters), ragged m / n / k, k >= 2048 (long-k rings)
-SHAPES = [(1, 2048 + 64, 1280 + 40, 2048 + 96), (3, 1024, 1024, 2048)]
+SHAPES = [(1, 2048 + 64, 1280 + 40, 2048 + 96), (3, 1024, 1024, 2048),
+          (1, 512, 4736, 2048),         # 74 tiles: every cluster resident, nothing to take over
+          (1, 768, 3200, 2048 + 32)]    # 75 tiles: one more than the resident clusters
 
 _RUN = r"""
 import sys, numpy as np
@@ -48,7 +50,7 @@ def _run(tmp_path, tag, env_clc, mode, batch, m, n, k, seed):
 
 
 @pytest.mark.parametrize("mode", ["fp16", "tf32"])
-@pytest.mark.parametrize("shape", SHAPES, ids=["ragged-99tiles", "batch3-96tiles"])
+@pytest.mark.parametrize("shape", SHAPES, ids=["ragged-99tiles", "batch3-96tiles", "74tiles", "75tiles"])
 def test_dynamic_tile_order_bit_identical(tmp_path, mode, shape):
     batch, m, n, k = shape
     seed = 11
@@ -62,3 +64,36 @@ def test_dynamic_tile_order_bit_identical(tmp_path, mode, shape):
     # the last row / column of the ragged edges too
     b, i, j = np.append(b, [batch - 1, 0]), np.append(i, [m - 1, m - 1]), np.append(j, [n - 1, 0])
     assert_bits_equal(c_dyn[b, j, i], oracle.emu_gemm_entries(mode, A, B, m, n, k, b, i, j, tc="sm100"))
+
+
+def test_dynamic_tile_order_two_streams():
+    """two long-k GEMMs launched on two streams at once: each grid's clusters take over
+    only their own grid's tiles (cluster launch control is per grid); both results equal
+    the same GEMMs run one after the other"""
+    import torch
+    import paper_2308_15152_b200 as emu
+    m, n, k, batch = 1024, 1280, 2048, 2
+    ops = [workloads.make_operands(batch, m, n, k, seed=s) for s in (21, 22)]
+    dev = [(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()) for A, B in ops]
+
+    def run(dA, dB, stream):
+        dC = torch.full((batch, n, m), float("nan"), device="cuda")
+        st = emu.emu_sgemm_batched(m, n, k, 1.0, dA, m, k * m, dB, k, n * k, 0.0, dC, m, n * m, batch, "fp16",
+                                   stream)
+        assert "long-k rings" in emu.emu_last_kernel_name()
+        return dC, st
+
+    ref = []
+    for dA, dB in dev:
+        dC, _ = run(dA, dB, torch.cuda.current_stream())
+        ref.append(dC)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        c1, _ = run(*dev[0], s1)
+    with torch.cuda.stream(s2):
+        c2, _ = run(*dev[1], s2)
+    torch.cuda.synchronize()
+    assert_bits_equal(c1.cpu().numpy(), ref[0].cpu().numpy())
+    assert_bits_equal(c2.cpu().numpy(), ref[1].cpu().numpy())
