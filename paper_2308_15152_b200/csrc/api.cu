@@ -500,7 +500,9 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
     // close together instead of drifting apart over the launch, so the panel is reused in L2:
     // c3 DRAM reads 70 -> 37 GB per launch (profiles/r02_summary.md)
     static const int clc_env = env_int("EMU_TS_CLC", 8, 0, 1 << 20);   // tuning only
-    p.clc = LONGK && !ASTAT && p.num_tiles <= (1LL << 30) ? clc_env : 0;   // streaming: units = tiles
+    static const int clc_as_env = env_int("EMU_TS_CLC_ASTAT", 0, 0, 1);   // tuning only
+    const long long units = ASTAT ? (long long)p.tiles_m * batch : p.num_tiles;
+    p.clc = (LONGK || (ASTAT && clc_as_env)) && units <= (1LL << 30) ? clc_env : 0;
     {
         // raster group: m-tiles per group walking the n-tiles together (EMU_GROUP_M, tuning);
         // dynamic order: 3 (each B panel is read by 3 row blocks close together)

@@ -81,7 +81,8 @@ struct PairTsCfg {
     static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
     // CLC (long-k streaming tiles, p.clc): two 16-byte cluster-launch-control responses
     // and their full / empty barriers precede the other barriers
-    static constexpr uint32_t CLC_BYTES = LONGK ? 32 + 8 * 6 : 0;
+    static constexpr bool DYN = LONGK || ASTAT;   // may take its units in the dynamic order
+    static constexpr uint32_t CLC_BYTES = DYN ? 32 + 8 * 6 : 0;
     static constexpr int CLC_CONSUMERS = 2 * 1 + 1 + 2 * 8 + 2 * 16;   // producer x2, MMA, splitter, combine warps
     static constexpr uint32_t BAR_BYTES = CLC_BYTES + 8 * (2 * S32 + 2 * SOP + 4 + ASLOTS) + 16;
     static constexpr uint32_t SMEM_BYTES = 1024 + S32 * F32_STAGE + SOP * OP_STAGE + CSTAGE_BYTES + BAR_BYTES;
@@ -179,7 +180,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     // tile order: static (cluster c takes units c, c + ncl, ...) or, with CLC, the unit of
     // each cluster launch this cluster cancels (in launch order: the clusters that share an
     // operand panel start it close together, so it is reused in L2)
-    const bool clc = Cfg::LONGK && p.clc != 0;
+    const bool clc = Cfg::DYN && p.clc != 0;
     auto clc_next = [&](uint32_t& ci, bool arrive) -> long long {
         const uint32_t slot = ci & 1u, ph = (ci >> 1) & 1u;
         ++ci;
@@ -210,7 +211,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             ptx::mbar_init(&acc_empty[i], 2 * Cfg::NUM_EPI_WARPS);
         }
         for (int i = 0; i < Cfg::ASLOTS; ++i) ptx::mbar_init(&aslot_empty[i], 1);
-        if (Cfg::LONGK) {
+        if (Cfg::DYN) {
             for (int i = 0; i < 2; ++i) {
                 ptx::mbar_init(&clc_full[i], 1);
                 ptx::mbar_init(&clc_empty[i], Cfg::CLC_CONSUMERS);
