@@ -36,6 +36,13 @@
 #include "sm100_ptx.cuh"
 #include "split.cuh"
 
+#ifndef EMU_TS_SOP16
+#define EMU_TS_SOP16 5   // FP16 operand slots (short k; tuning: -DEMU_TS_SOP16=n)
+#endif
+#ifndef EMU_TS_S32
+#define EMU_TS_S32 5     // FP32 stages at most (short k; tuning: -DEMU_TS_S32=n)
+#endif
+
 namespace emu {
 
 // LONGK_ (long-k streaming tiles, c3): no C staging area (the epilogue stores with
@@ -71,11 +78,11 @@ struct PairTsCfg {
     static constexpr int ASLOTS = (TMEM_COLS - A_COL0) / ACOLS;   // A stages TMEM holds
     // operand ring: B_hi/B_lo in shared memory (and the A stage in TMEM unless ASTAT);
     // FP16: 5 slots still leave room for 5 FP32 stages
-    static constexpr int SOP_MAX = MODE == 0 ? (LONGK ? 8 : 5) : 4;
+    static constexpr int SOP_MAX = MODE == 0 ? (LONGK ? 8 : EMU_TS_SOP16) : 4;
     static constexpr int SOP = ASLOTS < SOP_MAX ? ASLOTS : SOP_MAX;
     // FP32 stages: as many as fit next to the operand ring and C staging (<= 5)
     static constexpr int S32_FIT = (232448 - 2048 - SOP * OP_STAGE - CSTAGE_BYTES) / F32_STAGE;
-    static constexpr int S32_MAX = LONGK ? 6 : 5;
+    static constexpr int S32_MAX = LONGK ? 6 : EMU_TS_S32;
     static constexpr int S32 = S32_FIT < S32_MAX ? S32_FIT : S32_MAX;
     static constexpr uint32_t KCOLS = 8;                       // TMEM columns per MMA K step
     static_assert(A_COL0 + SOP * ACOLS <= TMEM_COLS, "TMEM budget");
