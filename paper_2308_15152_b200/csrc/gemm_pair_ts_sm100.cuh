@@ -42,6 +42,12 @@
 #ifndef EMU_TS_S32
 #define EMU_TS_S32 5     // FP32 stages at most (short k; tuning: -DEMU_TS_S32=n)
 #endif
+#ifndef EMU_TS_REGS_CTRL
+#define EMU_TS_REGS_CTRL 40    // setmaxnreg of the control / splitter warps (tuning)
+#endif
+#ifndef EMU_TS_REGS_SPLIT
+#define EMU_TS_REGS_SPLIT 56
+#endif
 
 namespace emu {
 
@@ -105,7 +111,8 @@ struct PairTsCfg {
     static constexpr int KS = BK / (NUM_SPLIT_WARPS / 4);   // k per splitter warp (A)
     static constexpr int ECOLS = BN / (NUM_EPI_WARPS / 4);  // accumulator columns per combine warp
     // SPLITC: the combine holds one part (D_corr) in registers while P1 runs
-    static constexpr uint32_t REGS_CTRL = 40, REGS_SPLIT = SPLITC ? 56 : 64, REGS_EPI = SPLITC ? 88 : 80;
+    static constexpr uint32_t REGS_CTRL = EMU_TS_REGS_CTRL, REGS_SPLIT = SPLITC ? EMU_TS_REGS_SPLIT : 64,
+                              REGS_EPI = SPLITC ? 88 : 80;
     static_assert(128 * REGS_CTRL + 32 * NUM_SPLIT_WARPS * REGS_SPLIT + 32 * NUM_EPI_WARPS * REGS_EPI <= 65536,
                   "register budget");
     static_assert(SMEM_BYTES <= 232448, "shared memory");
