@@ -21,7 +21,15 @@
 //             than clusters (twice the clusters at work; c4);
 //   BN =  96: 2 buffers (384 columns) -- the MMA of k-block j+1 overlaps the
 //             drain of k-block j (kept for comparison, EMU_TS_N=96).
+// (In this kernel, splitting a 128-wide tile's accumulators into two N = 64 groups was
+// much slower -- profiles/r02_summary.md.)
 // Streaming tiles load A with L2 evict_last and B with evict_first (p.l2_policy).
+// Long-k streaming tiles (LONGK) may take their tiles in a dynamic order (p.clc): the grid
+// has one cluster per tile, the resident clusters take over the others with cluster launch
+// control (a scheduler thread in the leader CTA claims the next tile p.clc k-stages before
+// the current tile's loads end and multicasts the response to both CTAs; every role reads
+// it from a 2-slot ring), so the row blocks of a raster group that read the same B panel
+// start it together and the panel is reused in L2 (c3 DRAM reads 70 -> ~35 GB per launch).
 // A-stationary (ASTAT, short k): the split A of a whole (batch item, 256-row block)
 // -- all k, hi and lo -- stays in TMEM (k <= 256 FP16, k <= 128 TF32) while the
 // cluster walks every n-tile of that row block, so A is loaded and split once per
