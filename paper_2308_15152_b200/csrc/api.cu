@@ -551,10 +551,12 @@ emu_status run_gemm_pair_ts(int dev, int sms, int m, int n, int k, float alpha, 
         if (le != cudaSuccess) return launch_status(le);
     }
     g_last_launches = 1;
-    g_last_kernel = kernel_name_once([](char* b, size_t nb) {
-        snprintf(b, nb, "emu_sgemm_pair_ts_kernel<%s, %d cols%s%s%s%s%s%s%s> (CTA pair, A in TMEM)",
+    // (the tile order is fixed per process: p.clc follows static tuning knobs)
+    const bool dyn = p.clc != 0;
+    g_last_kernel = kernel_name_once([dyn](char* b, size_t nb) {
+        snprintf(b, nb, "emu_sgemm_pair_ts_kernel<%s, %d cols%s%s%s%s%s%s%s%s> (CTA pair, A in TMEM)",
                  MODE == 0 ? "FP16" : "TF32", BN, SPLITC ? ", split commit" : "", ASTAT ? ", A-stationary" : "",
-                 Cfg::LONGK ? ", long-k rings" : "",
+                 Cfg::LONGK ? ", long-k rings" : "", dyn ? ", dynamic tile order" : "",
                  (RANGE & 2) ? ", range-safe" : "", (RANGE & 1) ? ", range flag" : "", TA ? ", op(A)=T" : "",
                  TB ? ", op(B)=T" : "");
     });

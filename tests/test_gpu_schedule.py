@@ -57,6 +57,7 @@ def test_dynamic_tile_order_bit_identical(tmp_path, mode, shape):
     c_dyn, name_dyn = _run(tmp_path, "dyn", None, mode, batch, m, n, k, seed)
     c_sta, name_sta = _run(tmp_path, "static", "0", mode, batch, m, n, k, seed)
     assert "long-k rings" in name_dyn and "long-k rings" in name_sta, (name_dyn, name_sta)
+    assert "dynamic tile order" in name_dyn and "dynamic tile order" not in name_sta, (name_dyn, name_sta)
     assert_bits_equal(c_dyn, c_sta)
     A, B = workloads.make_operands(batch, m, n, k, seed=seed)
     g = workloads.rng(seed + 1)
