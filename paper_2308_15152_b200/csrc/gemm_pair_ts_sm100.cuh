@@ -516,6 +516,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
         const uint32_t n = tid % Cfg::BNC, quarter = tid / Cfg::BNC;  // B: 8 k per thread (tid < B_THREADS)
         const bool has_b = tid < Cfg::B_THREADS;
         const uint32_t tq = tmem_base + ((q * 32u) << 16);
+        const uint32_t op_full_leader = ptx::mapa_shared(&op_full[0], 0);   // + 8 * slot
         uint32_t s32 = 0, ph32 = 0, sop = 0, phop = 0, unit_it = 0;
         uint32_t nonfinite = 0;
         const bool chk = (RANGE & 1) && p.range_flag != nullptr;   // the FP16 overflow flag was asked for
@@ -669,7 +670,7 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                     __syncwarp();
                     PROF_ADD(P_SPL_WORK);
                     if (lane == 0) {
-                        ptx::mbar_arrive_cluster(ptx::mapa_shared(&op_full[sop], 0));
+                        ptx::mbar_arrive_cluster(op_full_leader + 8 * sop);
                         ptx::mbar_arrive(&f32_empty[s32]);
                     }
                     if (warp == Cfg::SPLIT_WARP0 && lane == 0) TRACE_AT(2, 4, ks);
