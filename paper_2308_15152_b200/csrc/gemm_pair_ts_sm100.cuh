@@ -316,6 +316,9 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             // -------------------------------------------- MMA issuer (leader CTA only)
             if (rank == 0 && ptx::elect_one()) {
                 constexpr uint32_t idesc = ptx::instr_desc(MODE == 0 ? 0u : 2u, 0u, 0u, 256, Cfg::BN);
+                // B operand descriptor of slot 0, K step 0; slot s / step st / the lo part add their
+                // byte offsets >> 4 to the start-address field (shared memory < 256 KB: no carry)
+                const uint64_t dB0 = ptx::smem_desc(ptx::smem_u32(opbuf), 16, Cfg::B_SBO, Cfg::B_LAYOUT);
                 uint32_t s0 = 0, ph0 = 0, acc_it = 0;
                 if constexpr (Cfg::SPLITC) {
                     // per k-block: P2 + P3 into D_corr (barrier pair 1), then P1 into D_hi (pair 0)
@@ -338,13 +341,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                     if (!p.corr) return;
                                     const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
                                     const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
-                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+                                    const uint64_t dB_s = dB0 + (uint64_t)((s * Cfg::OP_STAGE) >> 4);
 #pragma unroll
                                     for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                        const uint64_t dB_hi =
-                                            ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                        const uint64_t dB_lo =
-                                            ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint64_t dB_hi = dB_s + (uint64_t)(st * 2);   // +32 bytes per K step
+                                        const uint64_t dB_lo = dB_s + (uint64_t)((Cfg::BOP_BYTES >> 4) + st * 2);
                                         const uint32_t ka = st * Cfg::KCOLS;
                                         const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
                                         if (MODE == 0) {
@@ -358,11 +359,10 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 };
                                 auto issue_hi = [&](int ks, uint32_t s) {
                                     const uint32_t a_hi = tmem_base + Cfg::A_COL0 + (ASTAT ? ks : s) * Cfg::ACOLS;
-                                    const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+                                    const uint64_t dB_s = dB0 + (uint64_t)((s * Cfg::OP_STAGE) >> 4);
 #pragma unroll
                                     for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                        const uint64_t dB_hi =
-                                            ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
+                                        const uint64_t dB_hi = dB_s + (uint64_t)(st * 2);
                                         const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
                                         if (MODE == 0)
                                             ptx::mma_f16_pair_ts(d_hi, a_hi + st * Cfg::KCOLS, dB_hi, idesc, acc);   // P1
@@ -457,12 +457,11 @@ emu_sgemm_pair_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
                                 PROF_T0();
                                 const uint32_t a_hi = tmem_base + Cfg::A_COL0 + s * Cfg::ACOLS;
                                 const uint32_t a_lo = a_hi + Cfg::ACOLS / 2;
-                                const uint32_t bbase = ptx::smem_u32(opbuf + s * Cfg::OP_STAGE);
+                                const uint64_t dB_s = dB0 + (uint64_t)((s * Cfg::OP_STAGE) >> 4);
 #pragma unroll
                                 for (int st = 0; st < Cfg::NSTEPS; ++st) {
-                                    const uint64_t dB_hi = ptx::smem_desc(bbase + st * 32, 16, Cfg::B_SBO, Cfg::B_LAYOUT);
-                                    const uint64_t dB_lo = ptx::smem_desc(bbase + Cfg::BOP_BYTES + st * 32, 16,
-                                                                          Cfg::B_SBO, Cfg::B_LAYOUT);
+                                    const uint64_t dB_hi = dB_s + (uint64_t)(st * 2);
+                                    const uint64_t dB_lo = dB_s + (uint64_t)((Cfg::BOP_BYTES >> 4) + st * 2);
                                     const uint32_t ka = st * Cfg::KCOLS;
                                     const uint32_t acc = (ks > ks0 || st > 0) ? 1u : 0u;
                                     if (MODE == 0) {
